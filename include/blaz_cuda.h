@@ -1,0 +1,178 @@
+/*
+ * blaz_cuda.h -- C ABI of the B200 (sm_100a) compressed-matrix library.
+ *
+ * Drop-in boundary for the reference's matrix API (namespace blaz,
+ * proj/include/blaz/matrix.hpp).  Plain pointers and sizes only; no C++ or
+ * torch types cross this boundary.  Two levels:
+ *
+ *   blz_*_dev   device-resident, stream-ordered, caller-owned buffers (the
+ *               throughput path; SoA compressed layout, see blz_cmat).
+ *   blz_*_host  host buffers in the reference's own in-memory layout (dense
+ *               row-major double, AoS 48-byte blz_block); copies in/out are part
+ *               of the call and the call is synchronous, like the reference's
+ *               value-returning functions.
+ *
+ * Every entry returns a blz_status.  On failure blz_last_error(ctx) holds the
+ * reference's exception message (e.g. "mat_add: dimension mismatch (16x16 vs
+ * 16x24)"); BLZ_INVALID_ARGUMENT maps to std::invalid_argument and
+ * BLZ_OUT_OF_RANGE to std::out_of_range (see include/blaz/blaz.hpp).
+ *
+ * Data-dependent errors found on the device (non-finite input to compress,
+ * "normalize: non-finite input", H/codec.hpp:21) are latched in the context:
+ * _host calls report them directly; after _dev calls use blz_ctx_sync().
+ *
+ * Exact mode (default): every kernel is compiled with -fmad=false and follows
+ * the reference's evaluation order, so phi/C are byte-exact and f/s/values
+ * bit-exact against the reference built with -ffp-contract=off.
+ */
+#ifndef BLAZ_CUDA_H
+#define BLAZ_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLZ_ABI_VERSION 1
+
+typedef enum blz_status {
+    BLZ_OK = 0,
+    BLZ_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    BLZ_OUT_OF_RANGE = 2,     /* std::out_of_range in the reference */
+    BLZ_CUDA_ERROR = 3,
+    BLZ_OUT_OF_MEMORY = 4,
+    BLZ_NOT_SUPPORTED = 5
+} blz_status;
+
+/* Reference compressed_block (H/block.hpp:33-38), 48 bytes in memory:
+ * first@0, slope@8, scale_factor@16, coeffs@17..44, 3 pad bytes. */
+typedef struct blz_block {
+    double first;
+    double slope;
+    uint8_t scale_factor;
+    int8_t coeffs[28];
+} blz_block;
+
+/* Device-resident compressed matrix, SoA over the row-major block grid
+ * (block (br,bc) is index br*block_cols+bc, as H/matrix.hpp:38-39).
+ * first/slope: nb doubles; scale: nb bytes; coeffs: nb*28 bytes, block t's
+ * 28 coefficients at coeffs[28*t .. 28*t+27] in the frozen keep-set order
+ * (H/block.hpp:48-56).  45 bytes per block, the on-disk payload size. */
+typedef struct blz_cmat {
+    uint64_t rows, cols;             /* logical dimensions */
+    uint64_t block_rows, block_cols; /* ceil(rows/8), ceil(cols/8) */
+    double* first;
+    double* slope;
+    uint8_t* scale;
+    int8_t* coeffs;
+} blz_cmat;
+
+typedef struct blz_ctx blz_ctx;
+
+/* GEMM accumulation modes for blz_matmul_* */
+typedef enum blz_gemm_mode {
+    BLZ_GEMM_EXACT = 0, /* DMUL+DADD, ascending k: bitwise equal to mat_mul/mat_dot */
+    BLZ_GEMM_FUSED = 1  /* DFMA, ascending k: tolerance parity (normwise) */
+} blz_gemm_mode;
+
+/* ---- context --------------------------------------------------------------- */
+int blz_abi_version(void);
+/* Creates a context on `device`.  `basis` may be NULL (the library evaluates
+ * the reference expression H/dct.hpp:17-21 with the host libm) or 64 doubles
+ * to upload bit-for-bit. */
+blz_status blz_ctx_create(int device, const double* basis, blz_ctx** out);
+void blz_ctx_destroy(blz_ctx* ctx);
+/* Stream for all subsequent calls (cudaStream_t as void*; NULL = legacy). */
+blz_status blz_ctx_set_stream(blz_ctx* ctx, void* stream);
+void* blz_ctx_get_stream(const blz_ctx* ctx);
+const char* blz_last_error(const blz_ctx* ctx);
+/* Synchronizes the context stream and reports latched device-side errors. */
+blz_status blz_ctx_sync(blz_ctx* ctx);
+/* Copies the 64-entry basis in use into `out`. */
+blz_status blz_ctx_basis(const blz_ctx* ctx, double* out);
+/* Number of kernel launches issued through this context so far. */
+uint64_t blz_ctx_launches(const blz_ctx* ctx);
+
+/* ---- device-resident compressed matrices --------------------------------- */
+/* Bytes of device memory one SoA matrix of rows x cols needs. */
+uint64_t blz_cmat_bytes(uint64_t rows, uint64_t cols);
+/* Lays out `m` over caller-owned device memory `mem` (blz_cmat_bytes bytes). */
+blz_status blz_cmat_view(uint64_t rows, uint64_t cols, void* mem, blz_cmat* m);
+/* Allocates with cudaMalloc (freed by blz_cmat_free). */
+blz_status blz_cmat_alloc(blz_ctx* ctx, uint64_t rows, uint64_t cols, blz_cmat* m);
+void blz_cmat_free(blz_ctx* ctx, blz_cmat* m);
+
+/* ---- device-level operations (stream-ordered, no hidden allocation) ------- */
+/* compress_matrix (H/matrix.hpp:97-111): dense row-major with leading
+ * dimension ld (elements); out must be rows x cols. */
+blz_status blz_compress_dev(blz_ctx* ctx, const double* dense, uint64_t rows, uint64_t cols,
+                            uint64_t ld, const blz_cmat* out);
+/* decompress_matrix (H/matrix.hpp:113-126): crops to rows x cols. */
+blz_status blz_decompress_dev(blz_ctx* ctx, const blz_cmat* in, double* dense, uint64_t ld);
+/* mat_add / mat_sub / mat_scale (H/matrix.hpp:128-151) */
+blz_status blz_add_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out);
+blz_status blz_sub_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out);
+blz_status blz_scale_dev(blz_ctx* ctx, const blz_cmat* a, double c, const blz_cmat* out);
+/* Batched mat_dot (H/matrix.hpp:157-173): out[q] = (Ahat Bhat)(i[q], j[q]).
+ * i, j, out are device arrays of n entries; indices are validated on device
+ * (an out-of-range index latches BLZ_OUT_OF_RANGE). */
+blz_status blz_dot_entries_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b,
+                               const uint64_t* i, const uint64_t* j, uint64_t n, double* out);
+/* Row-wise dot products (config 2; restated):
+ * r[i] = sum_j Ahat(i,j)*Bhat(i,j), ascending j from +0.0, for the rows of a
+ * and b (same dims).  r has a->rows entries. */
+blz_status blz_rowdot_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, double* r);
+/* Ascending serial sum of n doubles (the Frobenius total from row dots). */
+blz_status blz_sum_dev(blz_ctx* ctx, const double* v, uint64_t n, double* out);
+/* mat_mul (H/matrix.hpp:223-235) and mat_mul_dense (:239-250).
+ * scratch: device buffer of blz_matmul_scratch_bytes(a,b) bytes. */
+uint64_t blz_matmul_scratch_bytes(const blz_cmat* a, const blz_cmat* b);
+blz_status blz_matmul_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, int mode,
+                          void* scratch, const blz_cmat* out);
+blz_status blz_matmul_dense_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, int mode,
+                                void* scratch, double* out, uint64_t ld);
+/* AoS (48-byte blz_block, device memory) <-> SoA conversions. */
+blz_status blz_pack_aos_dev(blz_ctx* ctx, const blz_cmat* in, blz_block* out);
+blz_status blz_unpack_aos_dev(blz_ctx* ctx, const blz_block* in, const blz_cmat* out);
+
+/* ---- host-level drop-in entry points (synchronous) ------------------------ */
+/* Each mirrors one reference function; blocks are host AoS arrays of
+ * ceil(rows/8)*ceil(cols/8) entries.  `threads` is accepted for signature
+ * parity with the reference and ignored (there is no CPU fallback). */
+blz_status blz_compress_matrix(blz_ctx* ctx, const double* values, uint64_t rows, uint64_t cols,
+                               blz_block* out, unsigned threads);
+blz_status blz_decompress_matrix(blz_ctx* ctx, const blz_block* in, uint64_t rows, uint64_t cols,
+                                 double* out, unsigned threads);
+blz_status blz_mat_add(blz_ctx* ctx, const blz_block* a, uint64_t a_rows, uint64_t a_cols,
+                       const blz_block* b, uint64_t b_rows, uint64_t b_cols, blz_block* out,
+                       unsigned threads);
+blz_status blz_mat_sub(blz_ctx* ctx, const blz_block* a, uint64_t a_rows, uint64_t a_cols,
+                       const blz_block* b, uint64_t b_rows, uint64_t b_cols, blz_block* out,
+                       unsigned threads);
+blz_status blz_mat_scale(blz_ctx* ctx, const blz_block* a, uint64_t rows, uint64_t cols,
+                         double c, blz_block* out, unsigned threads);
+blz_status blz_mat_dot(blz_ctx* ctx, const blz_block* a, uint64_t a_rows, uint64_t a_cols,
+                       const blz_block* b, uint64_t b_rows, uint64_t b_cols, uint64_t i,
+                       uint64_t j, double* out);
+blz_status blz_mat_mul(blz_ctx* ctx, const blz_block* a, uint64_t a_rows, uint64_t a_cols,
+                       const blz_block* b, uint64_t b_rows, uint64_t b_cols, blz_block* out,
+                       unsigned threads);
+blz_status blz_mat_mul_dense(blz_ctx* ctx, const blz_block* a, uint64_t a_rows, uint64_t a_cols,
+                             const blz_block* b, uint64_t b_rows, uint64_t b_cols, double* out,
+                             unsigned threads);
+/* Config-2 restatement on host buffers: row dots r[rows] and their ascending
+ * total (*frob, may be NULL). */
+blz_status blz_mat_rowdot(blz_ctx* ctx, const blz_block* a, const blz_block* b, uint64_t rows,
+                          uint64_t cols, double* r, double* frob);
+
+/* ---- block-level entry points (H/codec.hpp, H/block_ops.hpp), batched ------ */
+/* n independent 8x8 blocks (64 row-major doubles each) <-> n blz_block. */
+blz_status blz_compress_blocks(blz_ctx* ctx, const double* tiles, uint64_t n, blz_block* out);
+blz_status blz_decompress_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, double* tiles);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLAZ_CUDA_H */

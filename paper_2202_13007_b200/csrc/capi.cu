@@ -1,0 +1,588 @@
+// capi.cu -- the C ABI (include/blaz_cuda.h) over the sm_100a kernels.
+//
+// Mirrors the reference's matrix API (proj/include/blaz/matrix.hpp): argument
+// checks, error categories and messages follow the reference line cited at
+// each check.  There is no CPU fallback: every numeric result comes from a
+// kernel launched here.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/blaz_cuda.h"
+#include "launch.h"
+
+static_assert(sizeof(blz_block) == 48, "blz_block must match blaz::compressed_block (48 B)");
+
+struct blz_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  blz::Basis basis{};
+  std::string err;
+  unsigned long long* d_err = nullptr;
+  uint64_t launches = 0;
+  int sm_count = 148;
+  // grow-only device scratch slots (host-level calls, add fallback worklist)
+  struct Slot {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  Slot slots[8];
+};
+
+namespace {
+
+enum SlotId { S_FB = 0, S_IN0, S_IN1, S_OUT, S_CM0, S_CM1, S_CM2, S_AUX };
+
+blz_status set_err(blz_ctx* c, blz_status st, const std::string& msg) {
+  if (c) c->err = msg;
+  return st;
+}
+
+blz_status cuda_err(blz_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return BLZ_OK;
+  if (e == cudaErrorMemoryAllocation)
+    return set_err(c, BLZ_OUT_OF_MEMORY, std::string(where) + ": " + cudaGetErrorString(e));
+  return set_err(c, BLZ_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define BLZ_CUDA(ctx, expr, where)                      \
+  do {                                                  \
+    cudaError_t e__ = (expr);                           \
+    if (e__ != cudaSuccess) return cuda_err(ctx, e__, where); \
+  } while (0)
+
+uint64_t nblk(uint64_t n) { return (n + 7) / 8; }
+
+blz::CMat view(const blz_cmat* m) {
+  return blz::CMat{m->rows, m->cols, m->block_rows, m->block_cols, m->first, m->slope, m->scale, m->coeffs};
+}
+
+blz::LaunchCtx lc(blz_ctx* c) { return blz::LaunchCtx{c->stream, c->d_err, &c->launches, c->sm_count}; }
+
+void* slot(blz_ctx* c, int id, size_t bytes, cudaError_t* e) {
+  auto& s = c->slots[id];
+  *e = cudaSuccess;
+  if (bytes == 0) bytes = 16;
+  if (s.bytes < bytes) {
+    if (s.p) {
+      cudaStreamSynchronize(c->stream);
+      cudaFree(s.p);
+      s.p = nullptr;
+      s.bytes = 0;
+    }
+    *e = cudaMalloc(&s.p, bytes);
+    if (*e != cudaSuccess) return nullptr;
+    s.bytes = bytes;
+  }
+  return s.p;
+}
+
+// H/dct.hpp:14-26, the same expression with the host libm.
+void reference_basis(double* t) {
+  const double pi = std::acos(-1.0);
+  for (int i = 0; i < 8; ++i) {
+    const double ai = (i == 0) ? std::sqrt(1.0 / 8.0) : std::sqrt(1.0 / 4.0);
+    for (int u = 0; u < 8; ++u) t[i * 8 + u] = ai * std::cos((2 * u + 1) * i * pi / 16.0);
+  }
+}
+
+blz_status check_cmat(blz_ctx* c, const blz_cmat* m, const char* what) {
+  if (!m) return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": null matrix");
+  if (m->block_rows != nblk(m->rows) || m->block_cols != nblk(m->cols))
+    return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": inconsistent block grid");
+  const uint64_t nb = m->block_rows * m->block_cols;
+  if (nb && (!m->first || !m->slope || !m->scale || !m->coeffs))
+    return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": null buffer");
+  return BLZ_OK;
+}
+
+// H/matrix.hpp:86-93
+blz_status same_dims(blz_ctx* c, uint64_t ar, uint64_t ac, uint64_t br, uint64_t bc, const char* what) {
+  if (ar != br || ac != bc)
+    return set_err(c, BLZ_INVALID_ARGUMENT,
+                   std::string(what) + ": dimension mismatch (" + std::to_string(ar) + "x" +
+                       std::to_string(ac) + " vs " + std::to_string(br) + "x" + std::to_string(bc) + ")");
+  return BLZ_OK;
+}
+
+blz_status latch_status(blz_ctx* c) {
+  unsigned long long v = ~0ull;
+  BLZ_CUDA(c, cudaMemcpyAsync(&v, c->d_err, sizeof v, cudaMemcpyDeviceToHost, c->stream), "error latch");
+  BLZ_CUDA(c, cudaStreamSynchronize(c->stream), "sync");
+  if (v == ~0ull) return BLZ_OK;
+  const unsigned long long reset = ~0ull;
+  BLZ_CUDA(c, cudaMemcpy(c->d_err, &reset, sizeof reset, cudaMemcpyHostToDevice), "error latch reset");
+  switch ((uint32_t)(v & 0xff)) {
+    case blz::DERR_NONFINITE_CODE:
+      return set_err(c, BLZ_INVALID_ARGUMENT, "normalize: non-finite input");
+    case blz::DERR_PREDICT_CODE:
+      return set_err(c, BLZ_INVALID_ARGUMENT, "predict: mean slope must be positive");
+    case blz::DERR_DOT_RANGE_CODE:
+      return set_err(c, BLZ_OUT_OF_RANGE, "mat_dot: index out of range");
+    default:
+      return set_err(c, BLZ_CUDA_ERROR, "unknown device error");
+  }
+}
+
+// Host-level helpers: a device SoA matrix laid over a scratch slot.
+blz_status scratch_cmat(blz_ctx* c, int id, uint64_t rows, uint64_t cols, blz_cmat* m) {
+  cudaError_t e;
+  void* p = slot(c, id, blz_cmat_bytes(rows, cols), &e);
+  if (!p) return cuda_err(c, e, "scratch allocation");
+  return blz_cmat_view(rows, cols, p, m);
+}
+
+blz_status upload_blocks(blz_ctx* c, const blz_block* h, uint64_t rows, uint64_t cols, int id, blz_cmat* m) {
+  blz_status st = scratch_cmat(c, id, rows, cols, m);
+  if (st) return st;
+  const uint64_t nb = m->block_rows * m->block_cols;
+  cudaError_t e;
+  void* aos = slot(c, S_AUX, nb * sizeof(blz_block), &e);
+  if (!aos) return cuda_err(c, e, "scratch allocation");
+  BLZ_CUDA(c, cudaMemcpyAsync(aos, h, nb * sizeof(blz_block), cudaMemcpyHostToDevice, c->stream), "H2D blocks");
+  return blz_unpack_aos_dev(c, (const blz_block*)aos, m);
+}
+
+blz_status download_blocks(blz_ctx* c, const blz_cmat* m, blz_block* h) {
+  const uint64_t nb = m->block_rows * m->block_cols;
+  cudaError_t e;
+  void* aos = slot(c, S_AUX, nb * sizeof(blz_block), &e);
+  if (!aos) return cuda_err(c, e, "scratch allocation");
+  blz_status st = blz_pack_aos_dev(c, m, (blz_block*)aos);
+  if (st) return st;
+  BLZ_CUDA(c, cudaMemcpyAsync(h, aos, nb * sizeof(blz_block), cudaMemcpyDeviceToHost, c->stream), "D2H blocks");
+  return BLZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int blz_abi_version(void) { return BLZ_ABI_VERSION; }
+
+blz_status blz_ctx_create(int device, const double* basis, blz_ctx** out) {
+  if (!out) return BLZ_INVALID_ARGUMENT;
+  *out = nullptr;
+  blz_ctx* c = new (std::nothrow) blz_ctx;
+  if (!c) return BLZ_OUT_OF_MEMORY;
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_err, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->d_err, 0xff, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    delete c;
+    return e == cudaErrorMemoryAllocation ? BLZ_OUT_OF_MEMORY : BLZ_CUDA_ERROR;
+  }
+  if (basis)
+    std::memcpy(c->basis.t, basis, sizeof c->basis.t);
+  else
+    reference_basis(c->basis.t);
+  *out = c;
+  return BLZ_OK;
+}
+
+void blz_ctx_destroy(blz_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& s : c->slots)
+    if (s.p) cudaFree(s.p);
+  if (c->d_err) cudaFree(c->d_err);
+  delete c;
+}
+
+blz_status blz_ctx_set_stream(blz_ctx* c, void* stream) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  c->stream = (cudaStream_t)stream;
+  return BLZ_OK;
+}
+
+void* blz_ctx_get_stream(const blz_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+const char* blz_last_error(const blz_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+blz_status blz_ctx_sync(blz_ctx* c) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  return latch_status(c);
+}
+
+blz_status blz_ctx_basis(const blz_ctx* c, double* out) {
+  if (!c || !out) return BLZ_INVALID_ARGUMENT;
+  std::memcpy(out, c->basis.t, sizeof c->basis.t);
+  return BLZ_OK;
+}
+
+uint64_t blz_ctx_launches(const blz_ctx* c) { return c ? c->launches : 0; }
+
+// ---- SoA matrices ----------------------------------------------------------
+static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
+
+uint64_t blz_cmat_bytes(uint64_t rows, uint64_t cols) {
+  const uint64_t nb = nblk(rows) * nblk(cols);
+  return align256(nb * 8) * 2 + align256(nb * 28) + align256(nb);
+}
+
+blz_status blz_cmat_view(uint64_t rows, uint64_t cols, void* mem, blz_cmat* m) {
+  if (!m) return BLZ_INVALID_ARGUMENT;
+  const uint64_t nb = nblk(rows) * nblk(cols);
+  char* p = (char*)mem;
+  m->rows = rows;
+  m->cols = cols;
+  m->block_rows = nblk(rows);
+  m->block_cols = nblk(cols);
+  m->first = (double*)p;
+  p += align256(nb * 8);
+  m->slope = (double*)p;
+  p += align256(nb * 8);
+  m->coeffs = (int8_t*)p;
+  p += align256(nb * 28);
+  m->scale = (uint8_t*)p;
+  return BLZ_OK;
+}
+
+blz_status blz_cmat_alloc(blz_ctx* c, uint64_t rows, uint64_t cols, blz_cmat* m) {
+  if (!c || !m) return BLZ_INVALID_ARGUMENT;
+  void* p = nullptr;
+  BLZ_CUDA(c, cudaMalloc(&p, blz_cmat_bytes(rows, cols)), "blz_cmat_alloc");
+  return blz_cmat_view(rows, cols, p, m);
+}
+
+void blz_cmat_free(blz_ctx* c, blz_cmat* m) {
+  (void)c;
+  if (m && m->first) cudaFree(m->first);
+  if (m) m->first = nullptr;
+}
+
+// ---- device-level operations -------------------------------------------------
+blz_status blz_compress_dev(blz_ctx* c, const double* dense, uint64_t rows, uint64_t cols, uint64_t ld,
+                            const blz_cmat* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (rows == 0 || cols == 0) return set_err(c, BLZ_INVALID_ARGUMENT, "compress_matrix: empty matrix");  // H/matrix.hpp:98
+  if (blz_status st = check_cmat(c, out, "compress_matrix")) return st;
+  if (out->rows != rows || out->cols != cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "compress_matrix: output dimension mismatch");
+  if (ld < cols) return set_err(c, BLZ_INVALID_ARGUMENT, "compress_matrix: ld < cols");
+  return cuda_err(c, blz::launch_compress(lc(c), c->basis, dense, rows, cols, ld, view(out)), "compress");
+}
+
+blz_status blz_decompress_dev(blz_ctx* c, const blz_cmat* in, double* dense, uint64_t ld) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, in, "decompress_matrix")) return st;
+  if (ld < in->cols) return set_err(c, BLZ_INVALID_ARGUMENT, "decompress_matrix: ld < cols");
+  if (in->block_rows * in->block_cols == 0) return BLZ_OK;
+  return cuda_err(c, blz::launch_decompress(lc(c), c->basis, view(in), dense, ld, in->rows, in->cols),
+                  "decompress");
+}
+
+static blz_status addsub_dev(blz_ctx* c, bool sub, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out) {
+  const char* what = sub ? "mat_sub" : "mat_add";
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, what)) return st;
+  if (blz_status st = check_cmat(c, b, what)) return st;
+  if (blz_status st = check_cmat(c, out, what)) return st;
+  if (blz_status st = same_dims(c, a->rows, a->cols, b->rows, b->cols, what)) return st;  // H/matrix.hpp:130
+  if (out->rows != a->rows || out->cols != a->cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": output dimension mismatch");
+  const uint64_t nb = a->block_rows * a->block_cols;
+  if (nb == 0) return BLZ_OK;
+  cudaError_t e;
+  void* fb = slot(c, S_FB, nb * sizeof(uint64_t) + 256, &e);
+  if (!fb) return cuda_err(c, e, "fallback worklist");
+  unsigned long long* cnt = (unsigned long long*)fb;
+  uint64_t* list = (uint64_t*)((char*)fb + 256);
+  return cuda_err(c, blz::launch_addsub(lc(c), c->basis, sub, view(a), view(b), view(out), list, cnt), what);
+}
+
+blz_status blz_add_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out) {
+  return addsub_dev(c, false, a, b, out);
+}
+blz_status blz_sub_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out) {
+  return addsub_dev(c, true, a, b, out);
+}
+
+blz_status blz_scale_dev(blz_ctx* c, const blz_cmat* a, double k, const blz_cmat* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "mat_scale")) return st;
+  if (blz_status st = check_cmat(c, out, "mat_scale")) return st;
+  if (out->rows != a->rows || out->cols != a->cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "mat_scale: output dimension mismatch");
+  const uint64_t nb = a->block_rows * a->block_cols;
+  if (nb == 0) return BLZ_OK;  // the reference never calls scale() on an empty grid
+  if (!std::isfinite(k)) return set_err(c, BLZ_INVALID_ARGUMENT, "scale: non-finite constant");  // H/block_ops.hpp:75
+  return cuda_err(c, blz::launch_scale(lc(c), view(a), k, view(out)), "mat_scale");
+}
+
+blz_status blz_dot_entries_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, const uint64_t* i,
+                               const uint64_t* j, uint64_t n, double* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "mat_dot")) return st;
+  if (blz_status st = check_cmat(c, b, "mat_dot")) return st;
+  if (a->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_dot: inner dimension mismatch");  // :159
+  return cuda_err(c, blz::launch_dot_entries(lc(c), c->basis, view(a), view(b), i, j, n, out), "mat_dot");
+}
+
+blz_status blz_rowdot_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, double* r) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "mat_rowdot")) return st;
+  if (blz_status st = check_cmat(c, b, "mat_rowdot")) return st;
+  if (blz_status st = same_dims(c, a->rows, a->cols, b->rows, b->cols, "mat_rowdot")) return st;
+  if (a->block_rows * a->block_cols == 0) return BLZ_OK;
+  return cuda_err(c, blz::launch_rowdot(lc(c), c->basis, view(a), view(b), r), "mat_rowdot");
+}
+
+blz_status blz_sum_dev(blz_ctx* c, const double* v, uint64_t n, double* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  return cuda_err(c, blz::launch_sum(lc(c), v, n, out), "sum");
+}
+
+uint64_t blz_matmul_scratch_bytes(const blz_cmat* a, const blz_cmat* b) {
+  if (!a || !b) return 0;
+  const uint64_t ma = 8 * a->block_rows, ka = 8 * a->block_cols, kb = 8 * b->block_rows, nb = 8 * b->block_cols;
+  return (ma * ka + kb * nb + ma * nb) * sizeof(double) + 256;
+}
+
+static blz_status matmul_common(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int mode, void* scratch,
+                                double** dc) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "mat_mul")) return st;
+  if (blz_status st = check_cmat(c, b, "mat_mul")) return st;
+  if (a->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: inner dimension mismatch");  // :207
+  if (mode != BLZ_GEMM_EXACT && mode != BLZ_GEMM_FUSED) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: bad mode");
+  if (!scratch) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: null scratch");
+  const uint64_t ma = 8 * a->block_rows, ka = 8 * a->block_cols, kb = 8 * b->block_rows, nn = 8 * b->block_cols;
+  double* da = (double*)scratch;
+  double* db = da + ma * ka;
+  *dc = db + kb * nn;
+  // decompress_tiles (H/matrix.hpp:178-183): full 8x8 tiles, padding included
+  auto L = lc(c);
+  BLZ_CUDA(c, blz::launch_decompress(L, c->basis, view(a), da, ka, ma, ka), "mat_mul decompress A");
+  BLZ_CUDA(c, blz::launch_decompress(L, c->basis, view(b), db, nn, kb, nn), "mat_mul decompress B");
+  BLZ_CUDA(c, blz::launch_gemm(L, mode, da, ka, db, nn, *dc, nn, ma, nn, a->cols), "mat_mul gemm");
+  return BLZ_OK;
+}
+
+blz_status blz_matmul_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int mode, void* scratch,
+                          const blz_cmat* out) {
+  double* dc = nullptr;
+  if (blz_status st = matmul_common(c, a, b, mode, scratch, &dc)) return st;
+  if (blz_status st = check_cmat(c, out, "mat_mul")) return st;
+  if (out->rows != a->rows || out->cols != b->cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: output dimension mismatch");
+  // each full accumulator tile compressed once (H/matrix.hpp:231-233)
+  const uint64_t ma = 8 * a->block_rows, nn = 8 * b->block_cols;
+  return cuda_err(c, blz::launch_compress(lc(c), c->basis, dc, ma, nn, nn, view(out)), "mat_mul compress");
+}
+
+blz_status blz_matmul_dense_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int mode, void* scratch,
+                                double* out, uint64_t ld) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "mat_mul")) return st;
+  if (blz_status st = check_cmat(c, b, "mat_mul")) return st;
+  if (a->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: inner dimension mismatch");
+  if (ld < b->cols) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul_dense: ld < cols");
+  if (!scratch) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: null scratch");
+  const uint64_t ma = 8 * a->block_rows, ka = 8 * a->block_cols, kb = 8 * b->block_rows, nn = 8 * b->block_cols;
+  double* da = (double*)scratch;
+  double* db = da + ma * ka;
+  auto L = lc(c);
+  BLZ_CUDA(c, blz::launch_decompress(L, c->basis, view(a), da, ka, ma, ka), "mat_mul decompress A");
+  BLZ_CUDA(c, blz::launch_decompress(L, c->basis, view(b), db, nn, kb, nn), "mat_mul decompress B");
+  // crop (H/matrix.hpp:242-248): entries outside a.rows x b.cols are never formed
+  BLZ_CUDA(c, blz::launch_gemm(L, mode, da, ka, db, nn, out, ld, a->rows, b->cols, a->cols), "mat_mul gemm");
+  return BLZ_OK;
+}
+
+blz_status blz_pack_aos_dev(blz_ctx* c, const blz_cmat* in, blz_block* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, in, "pack")) return st;
+  if (in->block_rows * in->block_cols == 0) return BLZ_OK;
+  return cuda_err(c, blz::launch_pack_aos(lc(c), view(in), out), "pack_aos");
+}
+
+blz_status blz_unpack_aos_dev(blz_ctx* c, const blz_block* in, const blz_cmat* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, out, "unpack")) return st;
+  if (out->block_rows * out->block_cols == 0) return BLZ_OK;
+  return cuda_err(c, blz::launch_unpack_aos(lc(c), in, view(out)), "unpack_aos");
+}
+
+// ---- host-level drop-in entry points ------------------------------------------
+blz_status blz_compress_matrix(blz_ctx* c, const double* values, uint64_t rows, uint64_t cols, blz_block* out,
+                               unsigned threads) {
+  (void)threads;
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (rows == 0 || cols == 0) return set_err(c, BLZ_INVALID_ARGUMENT, "compress_matrix: empty matrix");
+  cudaError_t e;
+  double* d = (double*)slot(c, S_IN0, rows * cols * sizeof(double), &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  BLZ_CUDA(c, cudaMemcpyAsync(d, values, rows * cols * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+  blz_cmat m;
+  if (blz_status st = scratch_cmat(c, S_CM0, rows, cols, &m)) return st;
+  if (blz_status st = blz_compress_dev(c, d, rows, cols, cols, &m)) return st;
+  if (blz_status st = download_blocks(c, &m, out)) return st;
+  return latch_status(c);
+}
+
+blz_status blz_decompress_matrix(blz_ctx* c, const blz_block* in, uint64_t rows, uint64_t cols, double* out,
+                                 unsigned threads) {
+  (void)threads;
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (rows == 0 || cols == 0) return BLZ_OK;
+  blz_cmat m;
+  if (blz_status st = upload_blocks(c, in, rows, cols, S_CM0, &m)) return st;
+  cudaError_t e;
+  double* d = (double*)slot(c, S_OUT, rows * cols * sizeof(double), &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  if (blz_status st = blz_decompress_dev(c, &m, d, cols)) return st;
+  BLZ_CUDA(c, cudaMemcpyAsync(out, d, rows * cols * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  return latch_status(c);
+}
+
+static blz_status mat_addsub_host(blz_ctx* c, bool sub, const blz_block* a, uint64_t ar, uint64_t ac,
+                                  const blz_block* b, uint64_t br, uint64_t bc, blz_block* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = same_dims(c, ar, ac, br, bc, sub ? "mat_sub" : "mat_add")) return st;
+  if (ar == 0 || ac == 0) return BLZ_OK;
+  blz_cmat ma, mb, mo;
+  if (blz_status st = upload_blocks(c, a, ar, ac, S_CM0, &ma)) return st;
+  if (blz_status st = upload_blocks(c, b, br, bc, S_CM1, &mb)) return st;
+  if (blz_status st = scratch_cmat(c, S_CM2, ar, ac, &mo)) return st;
+  if (blz_status st = addsub_dev(c, sub, &ma, &mb, &mo)) return st;
+  if (blz_status st = download_blocks(c, &mo, out)) return st;
+  return latch_status(c);
+}
+
+blz_status blz_mat_add(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac, const blz_block* b, uint64_t br,
+                       uint64_t bc, blz_block* out, unsigned threads) {
+  (void)threads;
+  return mat_addsub_host(c, false, a, ar, ac, b, br, bc, out);
+}
+
+blz_status blz_mat_sub(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac, const blz_block* b, uint64_t br,
+                       uint64_t bc, blz_block* out, unsigned threads) {
+  (void)threads;
+  return mat_addsub_host(c, true, a, ar, ac, b, br, bc, out);
+}
+
+blz_status blz_mat_scale(blz_ctx* c, const blz_block* a, uint64_t rows, uint64_t cols, double k, blz_block* out,
+                         unsigned threads) {
+  (void)threads;
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (rows == 0 || cols == 0) return BLZ_OK;
+  if (!std::isfinite(k)) return set_err(c, BLZ_INVALID_ARGUMENT, "scale: non-finite constant");
+  blz_cmat ma, mo;
+  if (blz_status st = upload_blocks(c, a, rows, cols, S_CM0, &ma)) return st;
+  if (blz_status st = scratch_cmat(c, S_CM2, rows, cols, &mo)) return st;
+  if (blz_status st = blz_scale_dev(c, &ma, k, &mo)) return st;
+  if (blz_status st = download_blocks(c, &mo, out)) return st;
+  return latch_status(c);
+}
+
+blz_status blz_mat_dot(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac, const blz_block* b, uint64_t br,
+                       uint64_t bc, uint64_t i, uint64_t j, double* out) {
+  if (!c || !out) return BLZ_INVALID_ARGUMENT;
+  if (ac != br) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_dot: inner dimension mismatch");  // H/matrix.hpp:159
+  if (i >= ar || j >= bc) return set_err(c, BLZ_OUT_OF_RANGE, "mat_dot: index out of range");  // :160
+  blz_cmat ma, mb;
+  if (blz_status st = upload_blocks(c, a, ar, ac, S_CM0, &ma)) return st;
+  if (blz_status st = upload_blocks(c, b, br, bc, S_CM1, &mb)) return st;
+  cudaError_t e;
+  uint64_t* q = (uint64_t*)slot(c, S_IN0, 4 * sizeof(uint64_t), &e);
+  if (!q) return cuda_err(c, e, "scratch allocation");
+  const uint64_t hq[2] = {i, j};
+  BLZ_CUDA(c, cudaMemcpyAsync(q, hq, sizeof hq, cudaMemcpyHostToDevice, c->stream), "H2D query");
+  double* d = (double*)(q + 2);
+  if (blz_status st = blz_dot_entries_dev(c, &ma, &mb, q, q + 1, 1, d)) return st;
+  BLZ_CUDA(c, cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  return latch_status(c);
+}
+
+static blz_status mat_mul_host(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac, const blz_block* b,
+                               uint64_t br, uint64_t bc, blz_block* out_c, double* out_d) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (ac != br) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: inner dimension mismatch");  // H/matrix.hpp:207
+  blz_cmat ma, mb;
+  if (blz_status st = upload_blocks(c, a, ar, ac, S_CM0, &ma)) return st;
+  if (blz_status st = upload_blocks(c, b, br, bc, S_CM1, &mb)) return st;
+  cudaError_t e;
+  void* scratch = slot(c, S_IN1, blz_matmul_scratch_bytes(&ma, &mb), &e);
+  if (!scratch) return cuda_err(c, e, "scratch allocation");
+  if (out_c) {
+    blz_cmat mo;
+    if (blz_status st = scratch_cmat(c, S_CM2, ar, bc, &mo)) return st;
+    if (blz_status st = blz_matmul_dev(c, &ma, &mb, BLZ_GEMM_EXACT, scratch, &mo)) return st;
+    if (blz_status st = download_blocks(c, &mo, out_c)) return st;
+  } else {
+    double* d = (double*)slot(c, S_OUT, ar * bc * sizeof(double), &e);
+    if (!d) return cuda_err(c, e, "scratch allocation");
+    if (blz_status st = blz_matmul_dense_dev(c, &ma, &mb, BLZ_GEMM_EXACT, scratch, d, bc)) return st;
+    BLZ_CUDA(c, cudaMemcpyAsync(out_d, d, ar * bc * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  }
+  return latch_status(c);
+}
+
+blz_status blz_mat_mul(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac, const blz_block* b, uint64_t br,
+                       uint64_t bc, blz_block* out, unsigned threads) {
+  (void)threads;
+  return mat_mul_host(c, a, ar, ac, b, br, bc, out, nullptr);
+}
+
+blz_status blz_mat_mul_dense(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac, const blz_block* b,
+                             uint64_t br, uint64_t bc, double* out, unsigned threads) {
+  (void)threads;
+  return mat_mul_host(c, a, ar, ac, b, br, bc, nullptr, out);
+}
+
+blz_status blz_mat_rowdot(blz_ctx* c, const blz_block* a, const blz_block* b, uint64_t rows, uint64_t cols,
+                          double* r, double* frob) {
+  if (!c || !r) return BLZ_INVALID_ARGUMENT;
+  if (rows == 0 || cols == 0) return BLZ_OK;
+  blz_cmat ma, mb;
+  if (blz_status st = upload_blocks(c, a, rows, cols, S_CM0, &ma)) return st;
+  if (blz_status st = upload_blocks(c, b, rows, cols, S_CM1, &mb)) return st;
+  cudaError_t e;
+  double* d = (double*)slot(c, S_OUT, (rows + 1) * sizeof(double), &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  if (blz_status st = blz_rowdot_dev(c, &ma, &mb, d)) return st;
+  if (frob)
+    if (blz_status st = blz_sum_dev(c, d, rows, d + rows)) return st;
+  BLZ_CUDA(c, cudaMemcpyAsync(r, d, rows * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  if (frob) BLZ_CUDA(c, cudaMemcpyAsync(frob, d + rows, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  return latch_status(c);
+}
+
+blz_status blz_compress_blocks(blz_ctx* c, const double* tiles, uint64_t n, blz_block* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (n == 0) return BLZ_OK;
+  // n tiles side by side form an 8 x 8n dense matrix with ld = 64 ... stored
+  // tile-major; view them as an (8n x 8) matrix: tile t = rows 8t..8t+7.
+  cudaError_t e;
+  double* d = (double*)slot(c, S_IN0, n * 64 * sizeof(double), &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  BLZ_CUDA(c, cudaMemcpyAsync(d, tiles, n * 64 * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+  blz_cmat m;
+  if (blz_status st = scratch_cmat(c, S_CM0, 8 * n, 8, &m)) return st;
+  if (blz_status st = blz_compress_dev(c, d, 8 * n, 8, 8, &m)) return st;
+  if (blz_status st = download_blocks(c, &m, out)) return st;
+  return latch_status(c);
+}
+
+blz_status blz_decompress_blocks(blz_ctx* c, const blz_block* in, uint64_t n, double* tiles) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (n == 0) return BLZ_OK;
+  blz_cmat m;
+  if (blz_status st = upload_blocks(c, in, 8 * n, 8, S_CM0, &m)) return st;
+  cudaError_t e;
+  double* d = (double*)slot(c, S_OUT, n * 64 * sizeof(double), &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  if (blz_status st = blz_decompress_dev(c, &m, d, 8)) return st;
+  BLZ_CUDA(c, cudaMemcpyAsync(tiles, d, n * 64 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  return latch_status(c);
+}
+
+}  // extern "C"

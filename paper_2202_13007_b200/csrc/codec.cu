@@ -1,0 +1,101 @@
+// codec.cu -- K1 compress / K2 decompress kernels (exact mode).
+//
+// compress_matrix (H/matrix.hpp:97-111) and decompress_matrix (:113-126):
+// one thread owns one 8x8 block of the row-major block grid; the per-block
+// arithmetic is blaz_device.cuh.
+#include "blaz_device.cuh"
+#include "launch.h"
+
+namespace blz {
+
+// Edge-replicated tile load (H/matrix.hpp:72-84).
+__device__ __forceinline__ void load_tile(const double* __restrict__ dense, uint64_t rows, uint64_t cols,
+                                          uint64_t ld, uint64_t bi, uint64_t bj, double (&m)[BC]) {
+  const uint64_t r0 = bi * BD, c0 = bj * BD;
+  if (r0 + BD <= rows && c0 + BD <= cols && ((ld | c0) & 1) == 0 &&
+      (reinterpret_cast<uintptr_t>(dense) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < BD; ++i) {
+      const double2* row = reinterpret_cast<const double2*>(dense + (r0 + i) * ld + c0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 v = __ldg(row + q);
+        m[i * BD + 2 * q] = v.x;
+        m[i * BD + 2 * q + 1] = v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < BD; ++i) {
+      const uint64_t r = min(r0 + i, rows - 1);
+#pragma unroll
+      for (int j = 0; j < BD; ++j) {
+        const uint64_t c = min(c0 + j, cols - 1);
+        m[i * BD + j] = __ldg(dense + r * ld + c);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) k_compress(const Basis B, const double* __restrict__ dense,
+                                                  uint64_t rows, uint64_t cols, uint64_t ld, CMat out,
+                                                  unsigned long long* err) {
+  const uint64_t nb = out.nb();
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t bi = t / out.bc, bj = t % out.bc;
+    double m[BC];
+    load_tile(dense, rows, cols, ld, bi, bj, m);
+    RBlock rb;
+    const uint32_t e = compress_exact(m, B, rb);
+    if (e != DERR_NONE) latch_error(err, t, e);
+    store_block(out, t, rb);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_decompress(const Basis B, CMat in, double* __restrict__ dense,
+                                                    uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
+  const uint64_t nb = in.nb();
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t bi = t / in.bc, bj = t % in.bc;
+    const RBlock rb = load_block(in, t);
+    const uint64_t r0 = bi * BD, c0 = bj * BD;
+    const bool full = r0 + BD <= crop_rows && c0 + BD <= crop_cols && ((ld | c0) & 1) == 0 &&
+                      (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+    decompress_exact(rb, B, [&](int u, const double (&row)[BD]) {
+      if (full) {
+        double2* dst = reinterpret_cast<double2*>(dense + (r0 + u) * ld + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_double2(row[2 * q], row[2 * q + 1]);
+      } else if (r0 + u < crop_rows) {
+#pragma unroll
+        for (int j = 0; j < BD; ++j)
+          if (c0 + j < crop_cols) dense[(r0 + u) * ld + c0 + j] = row[j];
+      }
+    });
+  }
+}
+
+static unsigned grid_for(uint64_t n, unsigned threads, int sms) {
+  const uint64_t want = (n + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)sms * 64;
+  return (unsigned)(want < cap ? (want ? want : 1) : cap);
+}
+
+cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
+                            uint64_t cols, uint64_t ld, const CMat& out) {
+  k_compress<<<grid_for(out.nb(), 128, c.sm_count), 128, 0, c.stream>>>(B, dense, rows, cols, ld, out, c.err);
+  ++*c.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
+                              uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
+  k_decompress<<<grid_for(in.nb(), 128, c.sm_count), 128, 0, c.stream>>>(B, in, dense, ld, crop_rows,
+                                                                        crop_cols);
+  ++*c.launches;
+  return cudaGetLastError();
+}
+
+}  // namespace blz

@@ -1,0 +1,38 @@
+// launch.h -- host-side launchers implemented by the kernel translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "blaz_types.h"
+
+namespace blz {
+
+struct LaunchCtx {
+  cudaStream_t stream;
+  unsigned long long* err;  // device error latch (lowest block index wins)
+  uint64_t* launches;       // host counter of kernel launches
+  int sm_count;
+};
+
+// codec.cu
+cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
+                            uint64_t cols, uint64_t ld, const CMat& out);
+cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
+                              uint64_t ld, uint64_t crop_rows, uint64_t crop_cols);
+// ops.cu
+cudaError_t launch_addsub(const LaunchCtx& c, const Basis& B, bool sub, const CMat& a, const CMat& b,
+                          const CMat& out, uint64_t* fb_list, unsigned long long* fb_count);
+cudaError_t launch_scale(const LaunchCtx& c, const CMat& a, double k, const CMat& out);
+cudaError_t launch_pack_aos(const LaunchCtx& c, const CMat& in, void* aos);
+cudaError_t launch_unpack_aos(const LaunchCtx& c, const void* aos, const CMat& out);
+// dot.cu
+cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
+                               const uint64_t* i, const uint64_t* j, uint64_t n, double* out);
+cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r);
+cudaError_t launch_sum(const LaunchCtx& c, const double* v, uint64_t n, double* out);
+// gemm.cu
+cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t lda, const double* Bm,
+                        uint64_t ldb, double* Cm, uint64_t ldc, uint64_t M, uint64_t N, uint64_t K);
+
+}  // namespace blz

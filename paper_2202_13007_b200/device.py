@@ -1,0 +1,211 @@
+"""Device-resident API: compressed matrices living in HBM (SoA, 45 B/block).
+
+Torch is used only for device memory and streams; every operation is one
+C-ABI call (``blz_*_dev``) that launches the sm_100a kernels on the context
+stream, which is bound to torch's current CUDA stream at each call.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .matrix import BLOCK_DTYPE, CompressedMatrix, Context
+
+
+def _nb(n: int) -> int:
+    return (n + 7) // 8
+
+
+_ctxs: dict[int, Context] = {}
+
+
+def context(device: int | None = None) -> Context:
+    dev = torch.cuda.current_device() if device is None else device
+    ctx = _ctxs.get(dev)
+    if ctx is None:
+        ctx = Context(dev)
+        _ctxs[dev] = ctx
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    return ctx
+
+
+class DeviceCMat:
+    """A blz_cmat laid over one torch uint8 buffer."""
+
+    def __init__(self, rows: int, cols: int, device=None, buf: torch.Tensor | None = None):
+        lib = N.load()
+        self.rows, self.cols = int(rows), int(cols)
+        nbytes = int(lib.blz_cmat_bytes(self.rows, self.cols))
+        if buf is None:
+            buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device or "cuda")
+        assert buf.numel() >= nbytes and buf.is_cuda
+        self.buf = buf
+        self.c = N.blz_cmat()
+        st = lib.blz_cmat_view(self.rows, self.cols, C.c_void_p(buf.data_ptr()), C.byref(self.c))
+        assert st == 0
+
+    @property
+    def block_rows(self):
+        return _nb(self.rows)
+
+    @property
+    def block_cols(self):
+        return _nb(self.cols)
+
+    @property
+    def nblocks(self):
+        return self.block_rows * self.block_cols
+
+    def ref(self):
+        return C.byref(self.c)
+
+    # SoA views (torch tensors aliasing the buffer)
+    def _view(self, ptr_attr: str, dtype, count):
+        off = getattr(self.c, ptr_attr) - self.buf.data_ptr()
+        item = torch.empty(0, dtype=dtype).element_size()
+        return self.buf[off:off + count * item].view(dtype)
+
+    @property
+    def first(self):
+        return self._view("first", torch.float64, self.nblocks)
+
+    @property
+    def slope(self):
+        return self._view("slope", torch.float64, self.nblocks)
+
+    @property
+    def scale(self):
+        return self._view("scale", torch.uint8, self.nblocks)
+
+    @property
+    def coeffs(self):
+        return self._view("coeffs", torch.int8, self.nblocks * 28).view(self.nblocks, 28)
+
+    def to_host(self, ctx: Context | None = None) -> CompressedMatrix:
+        ctx = ctx or context(self.buf.device.index)
+        aos = torch.empty(max(1, self.nblocks) * 48, dtype=torch.uint8, device=self.buf.device)
+        ctx.check(ctx.lib.blz_pack_aos_dev(ctx.handle, self.ref(), C.c_void_p(aos.data_ptr())))
+        host = aos.cpu().numpy().view(BLOCK_DTYPE)[: self.nblocks]
+        return CompressedMatrix(self.rows, self.cols, host.reshape(self.block_rows, self.block_cols).copy())
+
+    @staticmethod
+    def from_host(cm: CompressedMatrix, device="cuda", ctx: Context | None = None) -> "DeviceCMat":
+        out = DeviceCMat(cm.rows, cm.cols, device=device)
+        ctx = ctx or context(out.buf.device.index)
+        raw = np.ascontiguousarray(cm.blocks, BLOCK_DTYPE).view(np.uint8).reshape(-1)
+        aos = torch.from_numpy(raw.copy()).to(out.buf.device)
+        ctx.check(ctx.lib.blz_unpack_aos_dev(ctx.handle, C.c_void_p(aos.data_ptr()), out.ref()))
+        torch.cuda.current_stream(out.buf.device).synchronize()
+        return out
+
+
+def _ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def compress(dense: torch.Tensor, out: DeviceCMat | None = None) -> DeviceCMat:
+    """compress_matrix on a device fp64 2-D tensor (row stride = ld)."""
+    assert dense.is_cuda and dense.dtype == torch.float64 and dense.dim() == 2 and dense.stride(1) == 1
+    rows, cols = dense.shape
+    ctx = context(dense.device.index)
+    if rows == 0 or cols == 0:
+        raise N.InvalidArgument("compress_matrix: empty matrix")
+    out = out or DeviceCMat(rows, cols, device=dense.device)
+    ctx.check(ctx.lib.blz_compress_dev(ctx.handle, _ptr(dense), rows, cols, dense.stride(0), out.ref()))
+    return out
+
+
+def decompress(cm: DeviceCMat, out: torch.Tensor | None = None) -> torch.Tensor:
+    ctx = context(cm.buf.device.index)
+    if out is None:
+        out = torch.empty((cm.rows, cm.cols), dtype=torch.float64, device=cm.buf.device)
+    ctx.check(ctx.lib.blz_decompress_dev(ctx.handle, cm.ref(), _ptr(out), out.stride(0)))
+    return out
+
+
+def add(a: DeviceCMat, b: DeviceCMat, out: DeviceCMat | None = None) -> DeviceCMat:
+    ctx = context(a.buf.device.index)
+    out = out or DeviceCMat(a.rows, a.cols, device=a.buf.device)
+    ctx.check(ctx.lib.blz_add_dev(ctx.handle, a.ref(), b.ref(), out.ref()))
+    return out
+
+
+def sub(a: DeviceCMat, b: DeviceCMat, out: DeviceCMat | None = None) -> DeviceCMat:
+    ctx = context(a.buf.device.index)
+    out = out or DeviceCMat(a.rows, a.cols, device=a.buf.device)
+    ctx.check(ctx.lib.blz_sub_dev(ctx.handle, a.ref(), b.ref(), out.ref()))
+    return out
+
+
+def scale(a: DeviceCMat, c: float, out: DeviceCMat | None = None) -> DeviceCMat:
+    ctx = context(a.buf.device.index)
+    out = out or DeviceCMat(a.rows, a.cols, device=a.buf.device)
+    ctx.check(ctx.lib.blz_scale_dev(ctx.handle, a.ref(), C.c_double(c), out.ref()))
+    return out
+
+
+def dot_entries(a: DeviceCMat, b: DeviceCMat, i: torch.Tensor, j: torch.Tensor) -> torch.Tensor:
+    ctx = context(a.buf.device.index)
+    i = i.to(device=a.buf.device, dtype=torch.int64).contiguous()
+    j = j.to(device=a.buf.device, dtype=torch.int64).contiguous()
+    out = torch.empty(i.numel(), dtype=torch.float64, device=a.buf.device)
+    ctx.check(ctx.lib.blz_dot_entries_dev(ctx.handle, a.ref(), b.ref(), _ptr(i), _ptr(j), i.numel(), _ptr(out)))
+    return out
+
+
+def rowdot(a: DeviceCMat, b: DeviceCMat, out: torch.Tensor | None = None) -> torch.Tensor:
+    ctx = context(a.buf.device.index)
+    if out is None:
+        out = torch.empty(a.rows, dtype=torch.float64, device=a.buf.device)
+    ctx.check(ctx.lib.blz_rowdot_dev(ctx.handle, a.ref(), b.ref(), _ptr(out)))
+    return out
+
+
+def sum_ascending(v: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    ctx = context(v.device.index)
+    v = v.contiguous()
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=v.device)
+    ctx.check(ctx.lib.blz_sum_dev(ctx.handle, _ptr(v), v.numel(), _ptr(out)))
+    return out
+
+
+def frobenius(a: DeviceCMat, b: DeviceCMat):
+    r = rowdot(a, b)
+    return r, sum_ascending(r)
+
+
+def matmul_scratch(a: DeviceCMat, b: DeviceCMat) -> torch.Tensor:
+    n = int(N.load().blz_matmul_scratch_bytes(a.ref(), b.ref()))
+    return torch.empty(n, dtype=torch.uint8, device=a.buf.device)
+
+
+def matmul(a: DeviceCMat, b: DeviceCMat, mode: int = N.GEMM_EXACT, out: DeviceCMat | None = None,
+           scratch: torch.Tensor | None = None) -> DeviceCMat:
+    ctx = context(a.buf.device.index)
+    if a.cols != b.rows:
+        raise N.InvalidArgument("mat_mul: inner dimension mismatch")
+    scratch = scratch if scratch is not None else matmul_scratch(a, b)
+    out = out or DeviceCMat(a.rows, b.cols, device=a.buf.device)
+    ctx.check(ctx.lib.blz_matmul_dev(ctx.handle, a.ref(), b.ref(), mode, _ptr(scratch), out.ref()))
+    return out
+
+
+def matmul_dense(a: DeviceCMat, b: DeviceCMat, mode: int = N.GEMM_EXACT, out: torch.Tensor | None = None,
+                 scratch: torch.Tensor | None = None) -> torch.Tensor:
+    ctx = context(a.buf.device.index)
+    if a.cols != b.rows:
+        raise N.InvalidArgument("mat_mul: inner dimension mismatch")
+    scratch = scratch if scratch is not None else matmul_scratch(a, b)
+    if out is None:
+        out = torch.empty((a.rows, b.cols), dtype=torch.float64, device=a.buf.device)
+    ctx.check(ctx.lib.blz_matmul_dense_dev(ctx.handle, a.ref(), b.ref(), mode, _ptr(scratch), _ptr(out),
+                                           out.stride(0)))
+    return out
+
+
+def sync(device: int | None = None):
+    context(device).sync()

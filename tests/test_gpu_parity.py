@@ -1,0 +1,181 @@
+"""CUDA path vs the oracle / the reference's golden vectors (needs a B200).
+
+Bar: bit-exact.  phi and C[28] byte-exact, f, s and every decompressed /
+accumulated double bitwise equal to the reference compiled with
+-ffp-contract=off (the exact kernels are built with -fmad=false and follow the
+reference's evaluation order).  Calls go through the C ABI (libblaz_cuda.so).
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import bits, block_diff_report, blocks_equal
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU boxes deselect -m gpu
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2202_13007_b200 as blz  # noqa: E402
+from paper_2202_13007_b200 import device as dev  # noqa: E402
+from paper_2202_13007_b200 import workloads as W  # noqa: E402
+
+
+def cm_of(golden, n, key, rows, cols):
+    return blz.CompressedMatrix(rows, cols, golden[f"m{n}_{key}"])
+
+
+def test_basis_uploaded_bit_for_bit(golden):
+    ctx = blz.default_context()
+    assert np.array_equal(bits(ctx.basis()), bits(golden["basis"]))
+
+
+def test_golden_blocks(golden):
+    got = blz.compress_blocks(golden["tiles"])
+    assert blocks_equal(got, golden["tiles_c"]), block_diff_report(got, golden["tiles_c"])
+    dec = blz.decompress_blocks(golden["tiles_c"])
+    assert np.array_equal(bits(dec), bits(golden["tiles_d"]))
+
+
+def test_golden_ramp_known_answers(golden):
+    cb = blz.compress_block(golden["tiles"][0])
+    assert cb["scale_factor"] == 20
+    assert np.float64(cb["slope"]).view(np.uint64) == np.float64(0.04).view(np.uint64)
+
+
+def test_golden_pairs(golden):
+    pa, pb = golden["pair_a"], golden["pair_b"]
+    n = len(pa)
+    A = blz.CompressedMatrix(8 * n, 8, pa.reshape(n, 1))
+    B = blz.CompressedMatrix(8 * n, 8, pb.reshape(n, 1))
+    add = blz.mat_add(A, B).blocks.reshape(-1)
+    sub = blz.mat_sub(A, B).blocks.reshape(-1)
+    assert blocks_equal(add, golden["pair_add"]), block_diff_report(add, golden["pair_add"])
+    assert blocks_equal(sub, golden["pair_sub"]), block_diff_report(sub, golden["pair_sub"])
+
+
+@pytest.mark.parametrize("n", range(10))
+def test_golden_matrices(golden, n):
+    rows, cols = (int(v) for v in golden["shapes"][n])
+    g = lambda k: golden[f"m{n}_{k}"]  # noqa: E731
+    ca = blz.compress_matrix(g("a"))
+    assert blocks_equal(ca.blocks, g("ca")), block_diff_report(ca.blocks, g("ca"))
+    A, B, BT = cm_of(golden, n, "ca", rows, cols), cm_of(golden, n, "cb", rows, cols), cm_of(golden, n, "cbt", cols, rows)
+    assert np.array_equal(bits(blz.decompress_matrix(A)), bits(g("da")))
+    assert blocks_equal(blz.mat_add(A, B).blocks, g("add"))
+    assert blocks_equal(blz.mat_sub(A, B).blocks, g("sub"))
+    assert blocks_equal(blz.mat_scale(A, 3.5).blocks, g("scale"))
+    mul = blz.mat_mul(A, BT)
+    assert blocks_equal(mul.blocks, g("mul")), block_diff_report(mul.blocks, g("mul"))
+    assert np.array_equal(bits(blz.mat_mul_dense(A, BT)), bits(g("muld")))
+    dots = [blz.mat_dot(A, BT, int(i), int(j)) for i, j in zip(g("qi"), g("qj"))]
+    assert np.array_equal(bits(np.array(dots)), bits(g("dot")))
+    r, frob = blz.mat_rowdot(A, B)
+    assert np.array_equal(bits(r), bits(g("rowdot")))
+    assert np.float64(frob).view(np.uint64) == np.float64(g("frob")).view(np.uint64)
+
+
+# ---- config 0 at full size (1024 x 1024): every op vs the oracle -------------
+@pytest.fixture(scope="module")
+def cfg0(port):
+    a = W.smooth_field(1024, 1024, seed=1).numpy()
+    b = W.smooth_field(1024, 1024, seed=2).numpy()
+    return a, b, port.compress_matrix(a), port.compress_matrix(b)
+
+
+def test_cfg0_compress_decompress(cfg0, port):
+    a, b, oa, ob = cfg0
+    ca = blz.compress_matrix(a)
+    assert blocks_equal(ca.blocks, oa), block_diff_report(ca.blocks, oa)
+    assert np.array_equal(bits(blz.decompress_matrix(ca)), bits(port.decompress_matrix(oa, 1024, 1024)))
+
+
+def test_cfg0_add_sub_scale(cfg0, port):
+    a, b, oa, ob = cfg0
+    A, B = blz.CompressedMatrix(1024, 1024, oa), blz.CompressedMatrix(1024, 1024, ob)
+    for got, want in [(blz.mat_add(A, B).blocks, port.mat_add(oa, ob)),
+                      (blz.mat_sub(A, B).blocks, port.mat_sub(oa, ob)),
+                      (blz.mat_scale(A, 3.5).blocks, port.mat_scale(oa, 3.5))]:
+        assert blocks_equal(got, want), block_diff_report(got, want)
+
+
+def test_cfg0_device_api_matches_host_api(cfg0):
+    a, b, oa, ob = cfg0
+    da = dev.compress(torch.from_numpy(a).cuda())
+    db = dev.compress(torch.from_numpy(b).cuda())
+    s = dev.add(da, db)
+    host = s.to_host()
+    assert blocks_equal(host.blocks, blz.mat_add(blz.CompressedMatrix(1024, 1024, oa),
+                                                 blz.CompressedMatrix(1024, 1024, ob)).blocks)
+    back = dev.decompress(s).cpu().numpy()
+    assert np.array_equal(bits(back), bits(blz.decompress_matrix(host)))
+    dev.sync()
+
+
+# ---- ragged shapes and edge cases ---------------------------------------------
+@pytest.mark.parametrize("rows,cols", [(1, 1), (1, 64), (64, 1), (7, 9), (15, 17), (63, 65), (100, 3)])
+def test_ragged_shapes(port, rows, cols):
+    rng = np.random.default_rng(rows * 1000 + cols)
+    a = rng.normal(size=(rows, cols)).cumsum(axis=1)
+    ca = blz.compress_matrix(a)
+    oa = port.compress_matrix(a)
+    assert blocks_equal(ca.blocks, oa)
+    back = blz.decompress_matrix(ca)
+    assert back.shape == (rows, cols)
+    assert np.array_equal(bits(back), bits(port.decompress_matrix(oa, rows, cols)))
+
+
+def test_errors_match_reference():
+    with pytest.raises(blz.InvalidArgument, match="compress_matrix: empty matrix"):
+        blz.compress_matrix(np.zeros((0, 4)))
+    bad = np.ones((16, 16))
+    bad[9, 3] = np.inf
+    with pytest.raises(blz.InvalidArgument, match="normalize: non-finite input"):
+        blz.compress_matrix(bad)
+    a = blz.compress_matrix(np.ones((16, 16)))
+    b = blz.compress_matrix(np.ones((16, 24)))
+    with pytest.raises(blz.InvalidArgument, match=r"mat_add: dimension mismatch \(16x16 vs 16x24\)"):
+        blz.mat_add(a, b)
+    with pytest.raises(blz.InvalidArgument, match=r"mat_sub: dimension mismatch"):
+        blz.mat_sub(a, b)
+    with pytest.raises(blz.InvalidArgument, match="scale: non-finite constant"):
+        blz.mat_scale(a, float("nan"))
+    c = blz.compress_matrix(np.ones((24, 16)))
+    with pytest.raises(blz.InvalidArgument, match="mat_dot: inner dimension mismatch"):
+        blz.mat_dot(a, c, 0, 0)
+    with pytest.raises(blz.OutOfRange, match="mat_dot: index out of range"):
+        blz.mat_dot(a, a, 16, 0)
+    with pytest.raises(blz.InvalidArgument, match="mat_mul: inner dimension mismatch"):
+        blz.mat_mul(a, c)
+    # the context stays usable after errors
+    assert blz.compress_matrix(np.ones((8, 8))).blocks["first"][0, 0] == 1.0
+
+
+def test_identities(port):
+    rng = np.random.default_rng(7)
+    a = W.smooth_field(40, 56, seed=9).numpy()
+    ca = blz.compress_matrix(a)
+    assert blocks_equal(blz.mat_scale(ca, 1.0).blocks, ca.blocks)  # matrix_test.cpp:142-149
+    zero = blz.decompress_matrix(blz.mat_sub(ca, ca))  # matrix_test.cpp:151-156
+    assert not np.any(zero)
+    neg = blz.mat_scale(ca, -1.0)  # s1 + s2 == 0 -> dense fallback (block_ops_test.cpp:44-57)
+    out = blz.mat_add(ca, neg)
+    want = port.mat_add(ca.blocks, neg.blocks)
+    assert blocks_equal(out.blocks, want), block_diff_report(out.blocks, want)
+    z = blz.mat_scale(ca, 0.0)  # scale by 0 decompresses to zero (block_ops_test.cpp:96-101)
+    assert not np.any(blz.decompress_matrix(z))
+    b = blz.compress_matrix(rng.normal(size=(40, 56)))
+    assert blocks_equal(blz.mat_add(ca, b).blocks, blz.mat_add(b, ca).blocks)  # commutes bitwise
+
+
+def test_gemm_fused_mode_tolerance(port):
+    a = W.smooth_field(64, 96, seed=3).numpy()
+    b = W.smooth_field(96, 40, seed=4).numpy()
+    A, B = dev.compress(torch.from_numpy(a).cuda()), dev.compress(torch.from_numpy(b).cuda())
+    exact = dev.matmul_dense(A, B, mode=blz.GEMM_EXACT).cpu().numpy()
+    fused = dev.matmul_dense(A, B, mode=blz.GEMM_FUSED).cpu().numpy()
+    want = port.mat_mul_dense(A.to_host().blocks, 64, 96, B.to_host().blocks, 96, 40)
+    assert np.array_equal(bits(exact), bits(want))
+    # fused (DFMA) mode: normwise tolerance 1e-12 * max(1, ||ref||_inf) * K
+    err = np.max(np.abs(fused - want)) / max(1.0, np.max(np.abs(want)))
+    assert err <= 1e-12 * 96
