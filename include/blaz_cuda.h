@@ -94,6 +94,20 @@ blz_status blz_ctx_sync(blz_ctx* ctx);
 blz_status blz_ctx_basis(const blz_ctx* ctx, double* out);
 /* Number of kernel launches issued through this context so far. */
 uint64_t blz_ctx_launches(const blz_ctx* ctx);
+/* Kernel selection.  BLZ_MODE_DEFAULT: compress runs the verified fast path
+ * (fused arithmetic + certified integer decisions, uncertified blocks re-run in
+ * reference order -- results identical to the reference).  BLZ_MODE_EXACT:
+ * every kernel follows the reference's evaluation order literally. */
+#define BLZ_MODE_DEFAULT 0
+#define BLZ_MODE_EXACT 1
+blz_status blz_ctx_set_mode(blz_ctx* ctx, int mode);
+int blz_ctx_get_mode(const blz_ctx* ctx);
+/* 1 if the uploaded basis admits the verified fast path (the reference basis does). */
+int blz_ctx_fast_path_available(const blz_ctx* ctx);
+/* Cumulative counters (synchronizes): blocks compressed on the exact path
+ * because a decision was not certified, and add/sub blocks that took the
+ * s1 + s2 == 0 dense fallback (H/block_ops.hpp:36-44). */
+blz_status blz_ctx_stats(blz_ctx* ctx, uint64_t* compress_exact_blocks, uint64_t* addsub_fallback_blocks);
 
 /* ---- device-resident compressed matrices --------------------------------- */
 /* Bytes of device memory one SoA matrix of rows x cols needs. */

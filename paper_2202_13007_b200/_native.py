@@ -22,6 +22,7 @@ BLOCK_DTYPE = np.dtype(
 
 BLZ_OK, BLZ_INVALID_ARGUMENT, BLZ_OUT_OF_RANGE, BLZ_CUDA_ERROR, BLZ_OUT_OF_MEMORY, BLZ_NOT_SUPPORTED = range(6)
 GEMM_EXACT, GEMM_FUSED = 0, 1
+MODE_DEFAULT, MODE_EXACT = 0, 1
 
 
 class BlazError(RuntimeError):
@@ -63,6 +64,10 @@ SIGNATURES = {
     "blz_ctx_sync": (_ST, [_P]),
     "blz_ctx_basis": (_ST, [_P, _P]),
     "blz_ctx_launches": (_U64, [_P]),
+    "blz_ctx_set_mode": (_ST, [_P, _I]),
+    "blz_ctx_get_mode": (_I, [_P]),
+    "blz_ctx_fast_path_available": (_I, [_P]),
+    "blz_ctx_stats": (_ST, [_P, C.POINTER(_U64), C.POINTER(_U64)]),
     "blz_cmat_bytes": (_U64, [_U64, _U64]),
     "blz_cmat_view": (_ST, [_U64, _U64, _P, C.POINTER(blz_cmat)]),
     "blz_cmat_alloc": (_ST, [_P, _U64, _U64, C.POINTER(blz_cmat)]),

@@ -25,6 +25,12 @@ struct blz_ctx {
   unsigned long long* d_err = nullptr;
   uint64_t launches = 0;
   int sm_count = 148;
+  int mode = BLZ_MODE_DEFAULT;
+  bool fast_ok = false;        // basis admits the verified fast path
+  blz::FastInfo fast{};
+  unsigned long long* d_stats = nullptr;  // [0] compress exact-path blocks, [1] add/sub dense fallbacks
+  uint64_t* d_wl = nullptr;               // exact-path worklist: 256 B counter + capacity entries
+  uint64_t wl_cap = 0;
   // grow-only device scratch slots (host-level calls, add fallback worklist)
   struct Slot {
     void* p = nullptr;
@@ -35,7 +41,7 @@ struct blz_ctx {
 
 namespace {
 
-enum SlotId { S_FB = 0, S_IN0, S_IN1, S_OUT, S_CM0, S_CM1, S_CM2, S_AUX };
+enum SlotId { S_UNUSED = 0, S_IN0, S_IN1, S_OUT, S_CM0, S_CM1, S_CM2, S_AUX };
 
 blz_status set_err(blz_ctx* c, blz_status st, const std::string& msg) {
   if (c) c->err = msg;
@@ -61,7 +67,65 @@ blz::CMat view(const blz_cmat* m) {
   return blz::CMat{m->rows, m->cols, m->block_rows, m->block_cols, m->first, m->slope, m->scale, m->coeffs};
 }
 
-blz::LaunchCtx lc(blz_ctx* c) { return blz::LaunchCtx{c->stream, c->d_err, &c->launches, c->sm_count}; }
+blz::LaunchCtx lc(blz_ctx* c) {
+  blz::LaunchCtx L{};
+  L.stream = c->stream;
+  L.err = c->d_err;
+  L.launches = &c->launches;
+  L.sm_count = c->sm_count;
+  L.exact_only = (c->mode & BLZ_MODE_EXACT) != 0;
+  L.fast = c->fast_ok ? &c->fast : nullptr;
+  L.wl_count = (unsigned long long*)c->d_wl;
+  L.wl = c->d_wl ? c->d_wl + 32 : nullptr;
+  L.stats = c->d_stats;
+  return L;
+}
+
+// Grows the exact-path worklist to nb entries (grow-only; first large call only).
+blz_status ensure_worklist(blz_ctx* c, uint64_t nb) {
+  if (c->wl_cap >= nb && c->d_wl) return BLZ_OK;
+  if (c->d_wl) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_wl);
+    c->d_wl = nullptr;
+    c->wl_cap = 0;
+  }
+  const uint64_t cap = nb < 1024 ? 1024 : nb;
+  cudaError_t e = cudaMalloc(&c->d_wl, (cap + 32) * sizeof(uint64_t));
+  if (e != cudaSuccess) return cuda_err(c, e, "worklist allocation");
+  c->wl_cap = cap;
+  return BLZ_OK;
+}
+
+// The verified compress path relies on the basis being the orthonormal DCT-II
+// up to rounding: row abs sums <= sqrt(8)(1+1e-12) and the
+// off-DC entries of sigma sigma' tiny.  sigma_0^2 is summed in long double.
+void analyse_basis(blz_ctx* c) {
+  long double sig[8];
+  double rowabs = 0;
+  for (int i = 0; i < 8; ++i) {
+    long double acc = 0;
+    double ra = 0;
+    for (int u = 0; u < 8; ++u) {
+      acc += (long double)c->basis.t[i * 8 + u];
+      ra += std::fabs(c->basis.t[i * 8 + u]);
+    }
+    sig[i] = acc;
+    rowabs = ra > rowabs ? ra : rowabs;
+  }
+  long double off = 0;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j)
+      if (i || j) {
+        long double v = sig[i] * sig[j];
+        if (v < 0) v = -v;
+        off = v > off ? v : off;
+      }
+  c->fast.ss00 = (double)(sig[0] * sig[0]);
+  // the dropped lo*sigma_i*sigma_j terms are budgeted at 64 u |lo| in E_d
+  c->fast_ok = rowabs <= 2.8284271247461903 * (1.0 + 1e-12) && off <= 64.0 * 1.1102230246251565e-16 &&
+               std::fabs(c->fast.ss00 - 8.0) < 1e-12;
+}
 
 void* slot(blz_ctx* c, int id, size_t bytes, cudaError_t* e) {
   auto& s = c->slots[id];
@@ -174,6 +238,8 @@ blz_status blz_ctx_create(int device, const double* basis, blz_ctx** out) {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_err, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->d_err, 0xff, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_stats, 4 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->d_stats, 0, 4 * sizeof(unsigned long long));
   if (e != cudaSuccess) {
     delete c;
     return e == cudaErrorMemoryAllocation ? BLZ_OUT_OF_MEMORY : BLZ_CUDA_ERROR;
@@ -182,6 +248,7 @@ blz_status blz_ctx_create(int device, const double* basis, blz_ctx** out) {
     std::memcpy(c->basis.t, basis, sizeof c->basis.t);
   else
     reference_basis(c->basis.t);
+  analyse_basis(c);
   *out = c;
   return BLZ_OK;
 }
@@ -193,6 +260,8 @@ void blz_ctx_destroy(blz_ctx* c) {
   for (auto& s : c->slots)
     if (s.p) cudaFree(s.p);
   if (c->d_err) cudaFree(c->d_err);
+  if (c->d_stats) cudaFree(c->d_stats);
+  if (c->d_wl) cudaFree(c->d_wl);
   delete c;
 }
 
@@ -218,6 +287,27 @@ blz_status blz_ctx_basis(const blz_ctx* c, double* out) {
 }
 
 uint64_t blz_ctx_launches(const blz_ctx* c) { return c ? c->launches : 0; }
+
+blz_status blz_ctx_set_mode(blz_ctx* c, int mode) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (mode & ~(BLZ_MODE_EXACT)) return set_err(c, BLZ_INVALID_ARGUMENT, "blz_ctx_set_mode: unknown mode bits");
+  c->mode = mode;
+  return BLZ_OK;
+}
+
+int blz_ctx_get_mode(const blz_ctx* c) { return c ? c->mode : -1; }
+
+int blz_ctx_fast_path_available(const blz_ctx* c) { return c && c->fast_ok ? 1 : 0; }
+
+blz_status blz_ctx_stats(blz_ctx* c, uint64_t* compress_exact_blocks, uint64_t* addsub_fallback_blocks) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  unsigned long long h[4] = {0, 0, 0, 0};
+  BLZ_CUDA(c, cudaMemcpyAsync(h, c->d_stats, sizeof h, cudaMemcpyDeviceToHost, c->stream), "stats");
+  BLZ_CUDA(c, cudaStreamSynchronize(c->stream), "stats sync");
+  if (compress_exact_blocks) *compress_exact_blocks = h[0];
+  if (addsub_fallback_blocks) *addsub_fallback_blocks = h[1];
+  return BLZ_OK;
+}
 
 // ---- SoA matrices ----------------------------------------------------------
 static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
@@ -267,6 +357,7 @@ blz_status blz_compress_dev(blz_ctx* c, const double* dense, uint64_t rows, uint
   if (out->rows != rows || out->cols != cols)
     return set_err(c, BLZ_INVALID_ARGUMENT, "compress_matrix: output dimension mismatch");
   if (ld < cols) return set_err(c, BLZ_INVALID_ARGUMENT, "compress_matrix: ld < cols");
+  if (blz_status st = ensure_worklist(c, out->block_rows * out->block_cols)) return st;
   return cuda_err(c, blz::launch_compress(lc(c), c->basis, dense, rows, cols, ld, view(out)), "compress");
 }
 
@@ -290,12 +381,8 @@ static blz_status addsub_dev(blz_ctx* c, bool sub, const blz_cmat* a, const blz_
     return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": output dimension mismatch");
   const uint64_t nb = a->block_rows * a->block_cols;
   if (nb == 0) return BLZ_OK;
-  cudaError_t e;
-  void* fb = slot(c, S_FB, nb * sizeof(uint64_t) + 256, &e);
-  if (!fb) return cuda_err(c, e, "fallback worklist");
-  unsigned long long* cnt = (unsigned long long*)fb;
-  uint64_t* list = (uint64_t*)((char*)fb + 256);
-  return cuda_err(c, blz::launch_addsub(lc(c), c->basis, sub, view(a), view(b), view(out), list, cnt), what);
+  if (blz_status st = ensure_worklist(c, nb)) return st;
+  return cuda_err(c, blz::launch_addsub(lc(c), c->basis, sub, view(a), view(b), view(out)), what);
 }
 
 blz_status blz_add_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out) {
@@ -375,6 +462,7 @@ blz_status blz_matmul_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int 
     return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: output dimension mismatch");
   // each full accumulator tile compressed once (H/matrix.hpp:231-233)
   const uint64_t ma = 8 * a->block_rows, nn = 8 * b->block_cols;
+  if (blz_status st = ensure_worklist(c, a->block_rows * b->block_cols)) return st;
   return cuda_err(c, blz::launch_compress(lc(c), c->basis, dc, ma, nn, nn, view(out)), "mat_mul compress");
 }
 

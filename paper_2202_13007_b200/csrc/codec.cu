@@ -4,6 +4,7 @@
 // one thread owns one 8x8 block of the row-major block grid; the per-block
 // arithmetic is blaz_device.cuh.
 #include "blaz_device.cuh"
+#include "fastpath.cuh"
 #include "launch.h"
 
 namespace blz {
@@ -37,12 +38,58 @@ __device__ __forceinline__ void load_tile(const double* __restrict__ dense, uint
   }
 }
 
+// Exact compress (reference order) of every block -- mode BLZ_MODE_EXACT.
 __global__ void __launch_bounds__(128) k_compress(const Basis B, const double* __restrict__ dense,
                                                   uint64_t rows, uint64_t cols, uint64_t ld, CMat out,
                                                   unsigned long long* err) {
   const uint64_t nb = out.nb();
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
        t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t bi = t / out.bc, bj = t % out.bc;
+    double m[BC];
+    load_tile(dense, rows, cols, ld, bi, bj, m);
+    RBlock rb;
+    const uint32_t e = compress_exact(m, B, rb);
+    if (e != DERR_NONE) latch_error(err, t, e);
+    store_block(out, t, rb);
+  }
+}
+
+// Verified fast compress (fastpath.cuh); blocks whose decisions are not
+// certified are appended to the worklist for k_compress_worklist.
+__global__ void __launch_bounds__(128) k_compress_fast(const FastParams P, const double* __restrict__ dense,
+                                                       uint64_t rows, uint64_t cols, uint64_t ld, CMat out,
+                                                       unsigned long long* err, uint64_t* __restrict__ wl,
+                                                       unsigned long long* __restrict__ wl_count) {
+  const uint64_t nb = out.nb();
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t bi = t / out.bc, bj = t % out.bc;
+    double m[BC];
+    load_tile(dense, rows, cols, ld, bi, bj, m);
+    RBlock rb;
+    const uint32_t e = compress_fast(m, P, rb);
+    if (e == NEED_EXACT) {
+      wl[atomicAdd(wl_count, 1ull)] = t;
+      continue;
+    }
+    if (e != DERR_NONE) latch_error(err, t, e);
+    store_block(out, t, rb);
+  }
+}
+
+// Exact compress of the listed blocks (the certified-slow path).
+__global__ void __launch_bounds__(128) k_compress_worklist(const Basis B, const double* __restrict__ dense,
+                                                           uint64_t rows, uint64_t cols, uint64_t ld, CMat out,
+                                                           unsigned long long* err,
+                                                           const uint64_t* __restrict__ wl,
+                                                           const unsigned long long* __restrict__ wl_count,
+                                                           unsigned long long* stats) {
+  const uint64_t n = *wl_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(stats, (unsigned long long)n);
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = wl[q];
     const uint64_t bi = t / out.bc, bj = t % out.bc;
     double m[BC];
     load_tile(dense, rows, cols, ld, bi, bj, m);
@@ -85,8 +132,22 @@ static unsigned grid_for(uint64_t n, unsigned threads, int sms) {
 
 cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
                             uint64_t cols, uint64_t ld, const CMat& out) {
-  k_compress<<<grid_for(out.nb(), 128, c.sm_count), 128, 0, c.stream>>>(B, dense, rows, cols, ld, out, c.err);
-  ++*c.launches;
+  const unsigned g = grid_for(out.nb(), 128, c.sm_count);
+  if (c.exact_only || !c.fast) {
+    k_compress<<<g, 128, 0, c.stream>>>(B, dense, rows, cols, ld, out, c.err);
+    ++*c.launches;
+    return cudaGetLastError();
+  }
+  cudaError_t e = cudaMemsetAsync(c.wl_count, 0, sizeof(unsigned long long), c.stream);
+  if (e != cudaSuccess) return e;
+  FastParams P;
+  P.B = B;
+  P.ss00 = c.fast->ss00;
+  P.zero = 0;
+  k_compress_fast<<<g, 128, 0, c.stream>>>(P, dense, rows, cols, ld, out, c.err, c.wl, c.wl_count);
+  k_compress_worklist<<<c.sm_count, 128, 0, c.stream>>>(B, dense, rows, cols, ld, out, c.err, c.wl, c.wl_count,
+                                                        c.stats + 0);
+  *c.launches += 2;
   return cudaGetLastError();
 }
 

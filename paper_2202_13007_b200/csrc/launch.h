@@ -8,11 +8,20 @@
 
 namespace blz {
 
+struct FastInfo {
+  double ss00;  // RN(sigma_0^2) of the uploaded basis (extended-precision host sum)
+};
+
 struct LaunchCtx {
   cudaStream_t stream;
-  unsigned long long* err;  // device error latch (lowest block index wins)
-  uint64_t* launches;       // host counter of kernel launches
+  unsigned long long* err;       // device error latch (lowest block index wins)
+  uint64_t* launches;            // host counter of kernel launches
   int sm_count;
+  bool exact_only;               // BLZ_MODE_EXACT: reference-order kernels only
+  const FastInfo* fast;          // null when the basis does not admit the verified path
+  uint64_t* wl;                  // exact-path worklist (nb entries)
+  unsigned long long* wl_count;  // worklist length
+  unsigned long long* stats;     // [0] compress exact-path blocks, [1] add/sub dense-fallback blocks
 };
 
 // codec.cu
@@ -22,7 +31,7 @@ cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols);
 // ops.cu
 cudaError_t launch_addsub(const LaunchCtx& c, const Basis& B, bool sub, const CMat& a, const CMat& b,
-                          const CMat& out, uint64_t* fb_list, unsigned long long* fb_count);
+                          const CMat& out);
 cudaError_t launch_scale(const LaunchCtx& c, const CMat& a, double k, const CMat& out);
 cudaError_t launch_pack_aos(const LaunchCtx& c, const CMat& in, void* aos);
 cudaError_t launch_unpack_aos(const LaunchCtx& c, const void* aos, const CMat& out);

@@ -35,8 +35,9 @@ template <bool SUB>
 __global__ void __launch_bounds__(128) k_addsub_fallback(const Basis B, CMat a, CMat b, CMat out,
                                                          const uint64_t* __restrict__ fb_list,
                                                          const unsigned long long* __restrict__ fb_count,
-                                                         unsigned long long* err) {
+                                                         unsigned long long* err, unsigned long long* stats) {
   const uint64_t n = *fb_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(stats, (unsigned long long)n);
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
        q += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t t = fb_list[q];
@@ -125,19 +126,19 @@ static unsigned grid_for(uint64_t n, unsigned threads, int sms) {
 }
 
 cudaError_t launch_addsub(const LaunchCtx& c, const Basis& B, bool sub, const CMat& a, const CMat& b,
-                          const CMat& out, uint64_t* fb_list, unsigned long long* fb_count) {
-  cudaError_t e = cudaMemsetAsync(fb_count, 0, sizeof(unsigned long long), c.stream);
+                          const CMat& out) {
+  cudaError_t e = cudaMemsetAsync(c.wl_count, 0, sizeof(unsigned long long), c.stream);
   if (e != cudaSuccess) return e;
   const unsigned g = grid_for(out.nb(), 256, c.sm_count);
   if (sub)
-    k_addsub<true><<<g, 256, 0, c.stream>>>(a, b, out, fb_list, fb_count);
+    k_addsub<true><<<g, 256, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
   else
-    k_addsub<false><<<g, 256, 0, c.stream>>>(a, b, out, fb_list, fb_count);
+    k_addsub<false><<<g, 256, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
   const unsigned gf = (unsigned)c.sm_count;
   if (sub)
-    k_addsub_fallback<true><<<gf, 128, 0, c.stream>>>(B, a, b, out, fb_list, fb_count, c.err);
+    k_addsub_fallback<true><<<gf, 128, 0, c.stream>>>(B, a, b, out, c.wl, c.wl_count, c.err, c.stats + 1);
   else
-    k_addsub_fallback<false><<<gf, 128, 0, c.stream>>>(B, a, b, out, fb_list, fb_count, c.err);
+    k_addsub_fallback<false><<<gf, 128, 0, c.stream>>>(B, a, b, out, c.wl, c.wl_count, c.err, c.stats + 1);
   *c.launches += 2;
   return cudaGetLastError();
 }

@@ -87,6 +87,18 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.blz_ctx_launches(self.handle))
 
+    def set_mode(self, mode: int):
+        """MODE_DEFAULT (verified fast compress) or MODE_EXACT (reference order everywhere)."""
+        self.check(self.lib.blz_ctx_set_mode(self.handle, mode))
+
+    def fast_path_available(self) -> bool:
+        return bool(self.lib.blz_ctx_fast_path_available(self.handle))
+
+    def stats(self) -> dict:
+        a, b = C.c_uint64(), C.c_uint64()
+        self.check(self.lib.blz_ctx_stats(self.handle, C.byref(a), C.byref(b)))
+        return {"compress_exact_blocks": a.value, "addsub_fallback_blocks": b.value}
+
     def set_stream(self, stream_ptr: int | None):
         self.check(self.lib.blz_ctx_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 

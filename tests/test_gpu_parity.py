@@ -179,3 +179,61 @@ def test_gemm_fused_mode_tolerance(port):
     # fused (DFMA) mode: normwise tolerance 1e-12 * max(1, ||ref||_inf) * K
     err = np.max(np.abs(fused - want)) / max(1.0, np.max(np.abs(want)))
     assert err <= 1e-12 * 96
+
+
+# ---- verified fast path vs exact mode vs oracle --------------------------------
+def _adversarial_tiles(n_each=2000, seed=5):
+    rng = np.random.default_rng(seed)
+    tiles = []
+    tiles.append(rng.uniform(-100, 100, (n_each, 8, 8)))                       # rough
+    tiles.append(np.round(rng.uniform(-5, 5, (n_each, 8, 8))))                 # integer grids (ties)
+    tiles.append(np.round(rng.uniform(-5, 5, (n_each, 8, 8))) * 0.25)          # dyadic grids (ties)
+    x = np.arange(8.0)
+    ramp = x[:, None] * x[None, :]
+    tiles.append(ramp[None] * rng.integers(1, 50, (n_each, 1, 1)) / 100.0)     # scaled ramps
+    lin = rng.integers(-3, 4, (n_each, 1, 1)) * x[None, :, None] + rng.integers(-3, 4, (n_each, 1, 1)) * x[None, None, :]
+    tiles.append(lin.astype(np.float64))                                        # integer planes
+    mag = 10.0 ** rng.uniform(-300, 300, (n_each, 1, 1))
+    tiles.append(rng.normal(size=(n_each, 8, 8)).cumsum(axis=2) * mag)           # extreme magnitudes
+    tiles.append(1e18 + rng.uniform(0, 1e17, (n_each, 8, 8)))                   # INT64 conversion edge
+    sparse = np.zeros((n_each, 8, 8))
+    sparse[:, 3, 5] = rng.normal(size=n_each)
+    tiles.append(sparse)                                                        # one nonzero delta
+    const = np.broadcast_to(rng.normal(size=(n_each, 1, 1)), (n_each, 8, 8)).copy()
+    tiles.append(const)                                                         # constant blocks
+    return np.concatenate(tiles)
+
+
+def test_fast_path_matches_exact_and_oracle(port):
+    tiles = _adversarial_tiles()
+    n = tiles.shape[0]
+    dense = torch.from_numpy(tiles.reshape(n * 8, 8)).cuda()
+    ctx = dev.context()
+    assert ctx.fast_path_available()
+    before = ctx.stats()["compress_exact_blocks"]
+    fast = dev.compress(dense)
+    dev.sync()
+    used_exact = ctx.stats()["compress_exact_blocks"] - before
+    ctx.set_mode(blz.MODE_EXACT)
+    try:
+        exact = dev.compress(dense)
+        dev.sync()
+    finally:
+        ctx.set_mode(blz.MODE_DEFAULT)
+    hf, he = fast.to_host().blocks.reshape(-1), exact.to_host().blocks.reshape(-1)
+    want = port.compress_matrix(tiles.reshape(n * 8, 8)).reshape(-1)
+    assert blocks_equal(he, want), block_diff_report(he, want)
+    assert blocks_equal(hf, want), block_diff_report(hf, want)
+    # the exact path must stay the rare path even on these adversarial grids
+    assert used_exact < 0.25 * n, used_exact
+
+
+def test_fast_path_cfg1_sample(port):
+    a = W.quadratic_blocks(512, 4096, seed=21)
+    ctx = dev.context()
+    before = ctx.stats()["compress_exact_blocks"]
+    ca = dev.compress(a.cuda())
+    dev.sync()
+    used_exact = ctx.stats()["compress_exact_blocks"] - before
+    assert blocks_equal(ca.to_host().blocks, port.compress_matrix(a.numpy()))
+    assert used_exact <= 0.001 * ca.nblocks, used_exact
