@@ -186,14 +186,33 @@ __device__ __forceinline__ uint32_t compress_exact(double (&m)[BC], const Basis&
 // decompress_block (H/codec.hpp:150-185), exact, streamed row by row:
 // emit(u, row[8]) is called for u = 0..7 in order.
 // ---------------------------------------------------------------------------
+// C / phi, correctly rounded, for integer C in [-128, 127] and phi in [1, 255]:
+// r = RN(1/phi), q = RN(C*r), e = C - phi*q (exact in one FMA), RN(q + e*r).
+// Equal to the IEEE quotient over the whole 256 x 255 domain (checked
+// exhaustively, tests/test_oracle_golden.py::test_markstein_dequant_exhaustive).
+__device__ __forceinline__ double dequant(int c, double phi, double r) {
+  const double cd = (double)c;
+  const double q = cd * r;
+  const double e = fma(-phi, q, cd);
+  return fma(e, r, q);
+}
+
 template <class Emit>
 __device__ __forceinline__ void decompress_exact(const RBlock& b, const Basis& B, Emit&& emit) {
   const double s = b.s;
   double dq[KEPT];
   const bool zero = (s == 0.0);  // dequantize_prediction returns a zero grid (:151)
   const double fphi = (double)b.phi;
+  // phi in [1,255] (the reference reader rejects 0, H/io.hpp:129-130); other
+  // values take the IEEE division so that the result is still C / phi.
+  if (b.phi - 1u < 255u) {
+    const double r = 1.0 / fphi;
 #pragma unroll
-  for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : (double)get_coeff(b.c, k) / fphi;
+    for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : dequant(get_coeff(b.c, k), fphi, r);
+  } else {
+#pragma unroll
+    for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : (double)get_coeff(b.c, k) / fphi;
+  }
 
   double prev[BD];
 #pragma unroll

@@ -122,6 +122,11 @@ void analyse_basis(blz_ctx* c) {
         off = v > off ? v : off;
       }
   c->fast.ss00 = (double)(sig[0] * sig[0]);
+  {
+    const long double pi = 3.141592653589793238462643383279502884L;
+    c->fast.bfly[0] = (double)(1.0L / std::sqrt(8.0L));
+    for (int k = 1; k < 8; ++k) c->fast.bfly[k] = (double)(0.5L * std::cos((long double)k * pi / 16.0L));
+  }
   // the dropped lo*sigma_i*sigma_j terms are budgeted at 64 u |lo| in E_d
   c->fast_ok = rowabs <= 2.8284271247461903 * (1.0 + 1e-12) && off <= 64.0 * 1.1102230246251565e-16 &&
                std::fabs(c->fast.ss00 - 8.0) < 1e-12;

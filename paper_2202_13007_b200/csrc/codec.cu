@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(128) k_compress_worklist(const Basis B, const 
   }
 }
 
-__global__ void __launch_bounds__(128) k_decompress(const Basis B, CMat in, double* __restrict__ dense,
+__global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, double* __restrict__ dense,
                                                     uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
   const uint64_t nb = in.nb();
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
@@ -144,10 +144,11 @@ cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* de
   P.B = B;
   P.ss00 = c.fast->ss00;
   P.zero = 0;
-  k_compress_fast<<<g, 128, 0, c.stream>>>(P, dense, rows, cols, ld, out, c.err, c.wl, c.wl_count);
+  e = launch_compress_pair(c, P, dense, rows, cols, ld, out);
+  if (e != cudaSuccess) return e;
   k_compress_worklist<<<c.sm_count, 128, 0, c.stream>>>(B, dense, rows, cols, ld, out, c.err, c.wl, c.wl_count,
                                                         c.stats + 0);
-  *c.launches += 2;
+  *c.launches += 1;
   return cudaGetLastError();
 }
 

@@ -9,7 +9,8 @@
 namespace blz {
 
 struct FastInfo {
-  double ss00;  // RN(sigma_0^2) of the uploaded basis (extended-precision host sum)
+  double ss00;     // RN(sigma_0^2) of the uploaded basis (extended-precision host sum)
+  double bfly[8];  // 1/sqrt(8), cos(k pi/16)/2 for k = 1..7, correctly rounded
 };
 
 struct LaunchCtx {
@@ -24,6 +25,10 @@ struct LaunchCtx {
   unsigned long long* stats;     // [0] compress exact-path blocks, [1] add/sub dense-fallback blocks
 };
 
+// compress_pair.cu (verified fast path, two threads per block)
+struct FastParams;
+cudaError_t launch_compress_pair(const LaunchCtx& c, const FastParams& P, const double* dense, uint64_t rows,
+                                 uint64_t cols, uint64_t ld, const CMat& out);
 // codec.cu
 cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
                             uint64_t cols, uint64_t ld, const CMat& out);
