@@ -101,11 +101,14 @@ SIGNATURES = {
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Loads libblaz_cuda.so (raises NotBuilt when absent -- no fallback)."""
+def load(path: str | None = None):
+    """Loads libblaz_cuda.so (raises NotBuilt when absent -- no fallback).
+
+    BLZ_LIB_PATH overrides the in-tree library (A/B builds of the same ABI)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("BLZ_LIB_PATH") or LIB_PATH
     if not os.path.exists(path):
         raise NotBuilt(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = C.CDLL(path)

@@ -100,22 +100,29 @@ __global__ void __launch_bounds__(128) k_compress_worklist(const Basis B, const 
   }
 }
 
+// Warp-uniform loop (valid lanes predicated) so that the basis streams through
+// uniform registers (LDCU.128) rather than per-thread constant loads.
 __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, double* __restrict__ dense,
-                                                    uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
+                                                       uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
   const uint64_t nb = in.nb();
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t bi = t / in.bc, bj = t % in.bc;
-    const RBlock rb = load_block(in, t);
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+  for (uint64_t base = warp0 * 32; base < nb; base += nwarps * 32) {
+    const uint64_t t = base + lane;
+    const bool valid = t < nb;
+    const uint64_t tt = valid ? t : nb - 1;
+    const uint64_t bi = tt / in.bc, bj = tt % in.bc;
+    const RBlock rb = load_block(in, tt);
     const uint64_t r0 = bi * BD, c0 = bj * BD;
-    const bool full = r0 + BD <= crop_rows && c0 + BD <= crop_cols && ((ld | c0) & 1) == 0 &&
-                      (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+    const bool full = valid && aligned && r0 + BD <= crop_rows && c0 + BD <= crop_cols;
     decompress_exact(rb, B, [&](int u, const double (&row)[BD]) {
       if (full) {
         double2* dst = reinterpret_cast<double2*>(dense + (r0 + u) * ld + c0);
 #pragma unroll
         for (int q = 0; q < 4; ++q) dst[q] = make_double2(row[2 * q], row[2 * q + 1]);
-      } else if (r0 + u < crop_rows) {
+      } else if (valid && r0 + u < crop_rows) {
 #pragma unroll
         for (int j = 0; j < BD; ++j)
           if (c0 + j < crop_cols) dense[(r0 + u) * ld + c0 + j] = row[j];
