@@ -1,0 +1,274 @@
+// addsub.cu -- K3 add/sub and K4 scale over the SoA compressed layout.
+//
+// mat_add / mat_sub (H/matrix.hpp:128-144 -> H/block_ops.hpp:20-71).  A warp
+// owns 32 consecutive blocks: their records (f, s: 8 B; phi: 1 B; C: 28 B) are
+// loaded with coalesced 16-byte accesses into shared memory, combined per lane
+// with exactly the reference's arithmetic, staged and stored coalesced.
+//
+// Exactness of the integer steps without the conversion pipe:
+//  * int8 -> double: __hiloint2double(0x43300000, c ^ 0x80000000) - (2^52 + 2^31)
+//    is exact (one DADD);
+//  * round_half_away (H/block.hpp:61-67) for |x| < 2^50: k = RN_even(x) via
+//    x + 1.5*2^52, fr = x - k (exact, |fr| <= 1/2); at an exact tie (|fr| = 1/2
+//    with the sign of x) the reference rounds away from zero: k + sign(x).
+//    Larger |x| (only possible when s1 + s2 nearly cancels) use the
+//    reference's own truncation sequence (round_half_away in blaz_device.cuh).
+// The s1 + s2 == 0 dense fallback (:36-44) is handed to k_addsub_fallback via
+// the worklist, as before.
+#include "blaz_device.cuh"
+#include "fastpath.cuh"
+#include "launch.h"
+
+namespace blz {
+
+struct __align__(16) WarpRecs {
+  double f[32];
+  double s[32];
+  uint32_t c[32 * 7];
+  uint8_t phi[32];
+};
+
+__device__ __forceinline__ double i8_to_double(int c) {
+  return __hiloint2double(0x43300000, (int)((uint32_t)c ^ 0x80000000u)) - 4503601774854144.0;
+}
+
+// clamp_coeff(round_half_away(x)) (H/block.hpp:76-81), exact.
+// k = RN_even(x) (x + 1.5*2^52 - 1.5*2^52); at an exact tie |x - k| = 1/2 the
+// reference rounds away from zero, i.e. to x + copysign(1/2, x), which is an
+// exactly representable integer.  The integer is read from k + 1.5*2^52.
+__device__ __forceinline__ int clamp_coeff_fast(double x) {
+  const uint32_t hx = hi32(x);
+  if ((hx & 0x7FFFFFFFu) >= 0x43100000u) return clamp_coeff(x);  // |x| >= 2^50, inf, NaN
+  const double M = 6755399441055744.0;
+  double k = (x + M) - M;
+  if (fabs(x - k) == 0.5) k = x + __hiloint2double((int)((hx & 0x80000000u) | 0x3FE00000u), 0);
+  const int n = (int)lo32(k + M);
+  return min(max(n, -127), 127);
+}
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Starts the (coalesced, asynchronous) load of the 32 records starting at
+// block t0; the partial last group is loaded synchronously.
+__device__ __forceinline__ void load_recs(const CMat& m, uint64_t t0, uint64_t nb, int lane, WarpRecs& r) {
+  if (t0 + 32 <= nb) {
+    if (lane < 16)
+      cp16(&r.f[2 * lane], m.first + t0 + 2 * lane);
+    else
+      cp16(&r.s[2 * (lane - 16)], m.slope + t0 + 2 * (lane - 16));
+    if (lane < 2) cp16(&r.phi[16 * lane], m.scale + t0 + 16 * lane);
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(m.coeffs + t0 * 28);
+    uint8_t* dst = reinterpret_cast<uint8_t*>(r.c);
+    cp16(dst + 16 * lane, src + 16 * lane);
+    if (lane < 24) cp16(dst + 16 * (32 + lane), src + 16 * (32 + lane));
+  } else {
+    const uint64_t t = t0 + lane;
+    if (t < nb) {
+      r.f[lane] = m.first[t];
+      r.s[lane] = m.slope[t];
+      r.phi[lane] = m.scale[t];
+      const uint32_t* cw = reinterpret_cast<const uint32_t*>(m.coeffs + t * 28);
+#pragma unroll
+      for (int w = 0; w < 7; ++w) r.c[lane * 7 + w] = cw[w];
+    }
+  }
+}
+
+__device__ __forceinline__ void store_recs(const CMat& m, uint64_t t0, uint64_t nb, int lane, const WarpRecs& r) {
+  __syncwarp();
+  if (t0 + 32 <= nb) {
+    if (lane < 16) {
+      reinterpret_cast<double2*>(m.first + t0)[lane] = reinterpret_cast<const double2*>(r.f)[lane];
+    } else {
+      reinterpret_cast<double2*>(m.slope + t0)[lane - 16] = reinterpret_cast<const double2*>(r.s)[lane - 16];
+    }
+    m.scale[t0 + lane] = r.phi[lane];
+    const uint4* src = reinterpret_cast<const uint4*>(r.c);
+    uint4* dst = reinterpret_cast<uint4*>(m.coeffs + t0 * 28);
+    dst[lane] = src[lane];
+    if (lane < 24) dst[32 + lane] = src[32 + lane];
+  } else {
+    const uint64_t t = t0 + lane;
+    if (t < nb) {
+      m.first[t] = r.f[lane];
+      m.slope[t] = r.s[lane];
+      m.scale[t] = r.phi[lane];
+      uint32_t* cw = reinterpret_cast<uint32_t*>(m.coeffs + t * 28);
+#pragma unroll
+      for (int w = 0; w < 7; ++w) cw[w] = r.c[lane * 7 + w];
+    }
+  }
+}
+
+// Requires 16-byte aligned SoA arrays whose block offset is a multiple of 4
+// blocks (true for every blz_cmat_view-created matrix); the launcher checks.
+template <bool SUB>
+__global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uint64_t* __restrict__ wl,
+                                                   unsigned long long* __restrict__ wl_count) {
+  __shared__ __align__(16) WarpRecs sa[2][4], sb[2][4], so[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t nb = out.nb();
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  int buf = 0;
+  uint64_t t0 = gw * 32;
+  if (t0 < nb) {
+    load_recs(a, t0, nb, lane, sa[0][warp]);
+    load_recs(b, t0, nb, lane, sb[0][warp]);
+  }
+  cp_commit();
+  for (; t0 < nb; t0 += nw * 32) {
+    const uint64_t nx = t0 + nw * 32;
+    if (nx < nb) {  // prefetch the next group while this one is combined
+      load_recs(a, nx, nb, lane, sa[buf ^ 1][warp]);
+      load_recs(b, nx, nb, lane, sb[buf ^ 1][warp]);
+    }
+    cp_commit();
+    cp_wait1();
+    __syncwarp();
+    const WarpRecs& ra = sa[buf][warp];
+    const WarpRecs& rb = sb[buf][warp];
+    WarpRecs& ro = so[warp];
+    const uint64_t t = t0 + lane;
+    const double f1 = ra.f[lane], f2 = rb.f[lane], s1 = ra.s[lane], s2 = rb.s[lane];
+    const uint32_t p1 = ra.phi[lane], p2 = rb.phi[lane];
+    uint32_t c1[7], c2[7];
+#pragma unroll
+    for (int w = 0; w < 7; ++w) {
+      c1[w] = ra.c[lane * 7 + w];
+      c2[w] = rb.c[lane * 7 + w];
+    }
+    const double rhs = SUB ? -1.0 : 1.0;
+    double of = f1 + rhs * f2;  // (:22)
+    double os;
+    uint32_t ophi;
+    uint32_t oc[7];
+    bool fallback = false;
+    if (s2 == 0.0) {            // (:27)
+      os = s1;
+      ophi = p1;
+#pragma unroll
+      for (int w = 0; w < 7; ++w) oc[w] = c1[w];
+    } else if (s1 == 0.0) {     // (:28-33)
+      os = s2;
+      ophi = p2;
+#pragma unroll
+      for (int w = 0; w < 7; ++w) {
+        uint32_t r = c2[w];
+        if (SUB) {
+          r = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = (int)(int8_t)(uint8_t)(c2[w] >> (8 * q));
+            const int n = (c == -127) ? 127 : -c;
+            r |= (uint32_t)(n & 0xff) << (8 * q);
+          }
+        }
+        oc[w] = r;
+      }
+    } else {
+      os = s1 + s2;             // (:35)
+      fallback = (os == 0.0);   // (:36-44) -> worklist
+      const uint32_t phi = merge_scale_factor(p1, p2);
+      ophi = phi;
+      const double a1 = s1 / os;                          // (:51)
+      const double a2 = rhs * s2 / os;                    // (:52)
+      const double w1 = a1 / (double)p1 * (double)phi;    // (:53)
+      const double w2 = a2 / (double)p2 * (double)phi;    // (:54)
+#pragma unroll
+      for (int w = 0; w < 7; ++w) {
+        uint32_t r = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double x1 = (double)(int8_t)(uint8_t)(c1[w] >> (8 * q));  // I2F.F64.S8 on a byte lane
+          const double x2 = (double)(int8_t)(uint8_t)(c2[w] >> (8 * q));
+          const double v = w1 * x1 + w2 * x2;  // (:55-56)
+          r |= (uint32_t)(clamp_coeff_fast(v) & 0xff) << (8 * q);
+        }
+        oc[w] = r;
+      }
+    }
+    if (fallback && t < nb) wl[atomicAdd(wl_count, 1ull)] = t;
+    ro.f[lane] = of;
+    ro.s[lane] = os;
+    ro.phi[lane] = (uint8_t)ophi;
+#pragma unroll
+    for (int w = 0; w < 7; ++w) ro.c[lane * 7 + w] = oc[w];
+    store_recs(out, t0, nb, lane, ro);
+    __syncwarp();
+    buf ^= 1;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// mat_scale (H/block_ops.hpp:74-77): f*c, s*c; phi and C are copied, so the
+// kernel is three flat streams with 16-byte accesses.
+__global__ void __launch_bounds__(256) k_scale_v2(CMat a, double c, CMat out) {
+  const uint64_t nb = out.nb();
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  // f and s, two blocks per 16-byte access
+  const uint64_t n2 = nb / 2;
+  for (uint64_t i = tid; i < n2; i += nth) {
+    const double2 f = reinterpret_cast<const double2*>(a.first)[i];
+    const double2 s = reinterpret_cast<const double2*>(a.slope)[i];
+    reinterpret_cast<double2*>(out.first)[i] = make_double2(f.x * c, f.y * c);
+    reinterpret_cast<double2*>(out.slope)[i] = make_double2(s.x * c, s.y * c);
+  }
+  if ((nb & 1) && tid == 0) {
+    out.first[nb - 1] = a.first[nb - 1] * c;
+    out.slope[nb - 1] = a.slope[nb - 1] * c;
+  }
+  // coefficients: nb*28 bytes = nb*7/4 16-byte chunks (+ tail words)
+  const uint64_t cbytes = nb * 28;
+  const uint64_t n16 = cbytes / 16;
+  for (uint64_t i = tid; i < n16; i += nth)
+    reinterpret_cast<uint4*>(out.coeffs)[i] = reinterpret_cast<const uint4*>(a.coeffs)[i];
+  for (uint64_t i = n16 * 4 + tid; i < cbytes / 4; i += nth)
+    reinterpret_cast<uint32_t*>(out.coeffs)[i] = reinterpret_cast<const uint32_t*>(a.coeffs)[i];
+  // scale factors
+  const uint64_t np = nb / 16;
+  for (uint64_t i = tid; i < np; i += nth)
+    reinterpret_cast<uint4*>(out.scale)[i] = reinterpret_cast<const uint4*>(a.scale)[i];
+  for (uint64_t i = np * 16 + tid; i < nb; i += nth) out.scale[i] = a.scale[i];
+}
+
+static bool soa_aligned(const CMat& m) {
+  return ((reinterpret_cast<uintptr_t>(m.first) | reinterpret_cast<uintptr_t>(m.slope) |
+           reinterpret_cast<uintptr_t>(m.coeffs) | reinterpret_cast<uintptr_t>(m.scale)) & 15) == 0;
+}
+
+bool launch_addsub_v2(const LaunchCtx& c, bool sub, const CMat& a, const CMat& b, const CMat& out,
+                      cudaError_t* err) {
+  if (!soa_aligned(a) || !soa_aligned(b) || !soa_aligned(out)) return false;
+  const uint64_t warps = (out.nb() + 31) / 32;
+  const uint64_t want = (warps + 3) / 4;
+  const uint64_t cap = (uint64_t)c.sm_count * 6;
+  const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+  if (sub)
+    k_addsub_v2<true><<<g, 128, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
+  else
+    k_addsub_v2<false><<<g, 128, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
+  ++*c.launches;
+  *err = cudaGetLastError();
+  return true;
+}
+
+bool launch_scale_v2(const LaunchCtx& c, const CMat& a, double k, const CMat& out, cudaError_t* err) {
+  if (!soa_aligned(a) || !soa_aligned(out)) return false;
+  const uint64_t n16 = out.nb() * 28 / 16;
+  const uint64_t want = (n16 + 255) / 256;
+  const uint64_t cap = (uint64_t)c.sm_count * 16;
+  const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+  k_scale_v2<<<g, 256, 0, c.stream>>>(a, k, out);
+  ++*c.launches;
+  *err = cudaGetLastError();
+  return true;
+}
+
+}  // namespace blz

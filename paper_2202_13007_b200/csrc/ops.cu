@@ -130,10 +130,15 @@ cudaError_t launch_addsub(const LaunchCtx& c, const Basis& B, bool sub, const CM
   cudaError_t e = cudaMemsetAsync(c.wl_count, 0, sizeof(unsigned long long), c.stream);
   if (e != cudaSuccess) return e;
   const unsigned g = grid_for(out.nb(), 256, c.sm_count);
-  if (sub)
+  cudaError_t ev2 = cudaSuccess;
+  if (launch_addsub_v2(c, sub, a, b, out, &ev2)) {
+    if (ev2 != cudaSuccess) return ev2;
+    --*c.launches;  // counted again below with the fallback kernel
+  } else if (sub) {
     k_addsub<true><<<g, 256, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
-  else
+  } else {
     k_addsub<false><<<g, 256, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
+  }
   const unsigned gf = (unsigned)c.sm_count;
   if (sub)
     k_addsub_fallback<true><<<gf, 128, 0, c.stream>>>(B, a, b, out, c.wl, c.wl_count, c.err, c.stats + 1);
@@ -144,6 +149,8 @@ cudaError_t launch_addsub(const LaunchCtx& c, const Basis& B, bool sub, const CM
 }
 
 cudaError_t launch_scale(const LaunchCtx& c, const CMat& a, double k, const CMat& out) {
+  cudaError_t ev2 = cudaSuccess;
+  if (launch_scale_v2(c, a, k, out, &ev2)) return ev2;
   k_scale<<<grid_for(out.nb(), 256, c.sm_count), 256, 0, c.stream>>>(a, k, out);
   ++*c.launches;
   return cudaGetLastError();
