@@ -1,0 +1,333 @@
+// blaz/blaz.hpp -- C++ drop-in for the reference's public API, backed by the
+// sm_100a kernels of libblaz_cuda.so through the C ABI (include/blaz_cuda.h).
+//
+// A program written against the reference (proj/include/blaz/blaz.hpp) builds
+// against this header unchanged and links -lblaz_cuda: the same types
+// (block8, compressed_block, dense_matrix, compressed_matrix,
+// partial_reconstruction) with the same member layout, and the same functions
+// with the same signatures, exception types and messages:
+//
+//   compress_matrix / decompress_matrix      H/matrix.hpp:97-126
+//   mat_add / mat_sub / mat_scale            H/matrix.hpp:128-151
+//   mat_dot                                  H/matrix.hpp:157-173
+//   mat_mul / mat_mul_dense                  H/matrix.hpp:223-250
+//   compress_block / decompress_block        H/codec.hpp:130-146, :180-185
+//   dequantize_prediction                    H/codec.hpp:150-158
+//   add / sub / scale / dot / block_mul      H/block_ops.hpp:65-142
+//   reconstruct_rows / reconstruct_cols      H/block_ops.hpp:87-115
+//   ref::add/sub/scale/dot/mul               H/matrix.hpp:253-300 (dense baselines)
+//
+// Every compressed-domain result is computed on the GPU (one process-wide
+// context on device $BLZ_DEVICE, default 0); `threads` is accepted and ignored.
+// The ref:: functions are the reference's uncompressed CPU baselines, kept for
+// source compatibility of benchmarks and tests.
+#ifndef BLAZ_DROPIN_BLAZ_HPP
+#define BLAZ_DROPIN_BLAZ_HPP
+
+#include <array>
+#include <cmath>
+#include <cstddef>
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../blaz_cuda.h"
+
+namespace blaz {
+
+inline constexpr int block_dim = 8;
+inline constexpr int block_cells = block_dim * block_dim;
+inline constexpr int kept_coeff_count = 28;
+inline constexpr int block_payload_bytes = 8 + 8 + 1 + kept_coeff_count;
+inline constexpr double compression_rate =
+    double(block_cells * 8 * 8) / double(block_payload_bytes * 8);
+
+struct block8 {
+    std::array<double, block_cells> a{};
+    double& operator()(int r, int c) { return a[r * block_dim + c]; }
+    const double& operator()(int r, int c) const { return a[r * block_dim + c]; }
+};
+
+struct compressed_block {
+    double first = 0.0;
+    double slope = 0.0;
+    std::uint8_t scale_factor = 1;
+    std::array<std::int8_t, kept_coeff_count> coeffs{};
+};
+static_assert(sizeof(compressed_block) == sizeof(blz_block), "48-byte AoS record");
+static_assert(offsetof(compressed_block, scale_factor) == offsetof(blz_block, scale_factor), "layout");
+static_assert(offsetof(compressed_block, coeffs) == offsetof(blz_block, coeffs), "layout");
+
+struct coeff_position {
+    std::uint8_t row;
+    std::uint8_t col;
+};
+
+// Frozen keep-set order: row 0, row 1, column 0 rows 2..7, column 1 rows 2..7.
+inline constexpr std::array<coeff_position, kept_coeff_count> kept_coeff_positions = [] {
+    std::array<coeff_position, kept_coeff_count> p{};
+    for (int k = 0; k < kept_coeff_count; ++k) {
+        if (k < 16) p[k] = {std::uint8_t(k / 8), std::uint8_t(k % 8)};
+        else if (k < 22) p[k] = {std::uint8_t(k - 14), 0};
+        else p[k] = {std::uint8_t(k - 20), 1};
+    }
+    return p;
+}();
+
+struct dense_matrix {
+    std::size_t rows = 0;
+    std::size_t cols = 0;
+    std::vector<double> values;
+
+    dense_matrix() = default;
+    dense_matrix(std::size_t r, std::size_t c) : rows(r), cols(c), values(r * c, 0.0) {}
+    double& operator()(std::size_t r, std::size_t c) { return values[r * cols + c]; }
+    const double& operator()(std::size_t r, std::size_t c) const { return values[r * cols + c]; }
+};
+
+struct compressed_matrix {
+    std::size_t rows = 0;
+    std::size_t cols = 0;
+    std::size_t block_rows = 0;
+    std::size_t block_cols = 0;
+    std::vector<compressed_block> blocks;
+
+    compressed_block& block(std::size_t br, std::size_t bc) { return blocks[br * block_cols + bc]; }
+    const compressed_block& block(std::size_t br, std::size_t bc) const { return blocks[br * block_cols + bc]; }
+};
+
+struct partial_reconstruction {
+    block8 values;
+    int extent = 0;
+};
+
+namespace gpu {
+
+// Process-wide context (created on first use).
+inline blz_ctx* context() {
+    static std::once_flag once;
+    static blz_ctx* ctx = nullptr;
+    std::call_once(once, [] {
+        const char* d = std::getenv("BLZ_DEVICE");
+        if (blz_ctx_create(d ? std::atoi(d) : 0, nullptr, &ctx) != BLZ_OK)
+            throw std::runtime_error("blaz: cannot create the CUDA context");
+    });
+    return ctx;
+}
+
+inline void check(blz_status st) {
+    if (st == BLZ_OK) return;
+    const std::string msg = blz_last_error(context());
+    if (st == BLZ_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    if (st == BLZ_OUT_OF_RANGE) throw std::out_of_range(msg);
+    if (st == BLZ_OUT_OF_MEMORY) throw std::bad_alloc();
+    throw std::runtime_error("blaz: " + msg);
+}
+
+inline blz_block* raw(compressed_block* b) { return reinterpret_cast<blz_block*>(b); }
+inline const blz_block* raw(const compressed_block* b) { return reinterpret_cast<const blz_block*>(b); }
+
+inline compressed_matrix shaped(std::size_t rows, std::size_t cols) {
+    compressed_matrix m;
+    m.rows = rows;
+    m.cols = cols;
+    m.block_rows = (rows + block_dim - 1) / block_dim;
+    m.block_cols = (cols + block_dim - 1) / block_dim;
+    m.blocks.resize(m.block_rows * m.block_cols);
+    return m;
+}
+
+}  // namespace gpu
+
+// ---- matrix level ------------------------------------------------------------
+inline compressed_matrix compress_matrix(const dense_matrix& m, unsigned threads = 1) {
+    if (m.rows == 0 || m.cols == 0) throw std::invalid_argument("compress_matrix: empty matrix");
+    compressed_matrix cm = gpu::shaped(m.rows, m.cols);
+    gpu::check(blz_compress_matrix(gpu::context(), m.values.data(), m.rows, m.cols, gpu::raw(cm.blocks.data()),
+                                   threads));
+    return cm;
+}
+
+inline dense_matrix decompress_matrix(const compressed_matrix& cm, unsigned threads = 1) {
+    dense_matrix m(cm.rows, cm.cols);
+    if (cm.blocks.empty()) return m;
+    gpu::check(blz_decompress_matrix(gpu::context(), gpu::raw(cm.blocks.data()), cm.rows, cm.cols,
+                                     m.values.data(), threads));
+    return m;
+}
+
+inline compressed_matrix mat_add(const compressed_matrix& a, const compressed_matrix& b, unsigned threads = 1) {
+    compressed_matrix out = gpu::shaped(a.rows, a.cols);
+    gpu::check(blz_mat_add(gpu::context(), gpu::raw(a.blocks.data()), a.rows, a.cols, gpu::raw(b.blocks.data()),
+                           b.rows, b.cols, gpu::raw(out.blocks.data()), threads));
+    return out;
+}
+
+inline compressed_matrix mat_sub(const compressed_matrix& a, const compressed_matrix& b, unsigned threads = 1) {
+    compressed_matrix out = gpu::shaped(a.rows, a.cols);
+    gpu::check(blz_mat_sub(gpu::context(), gpu::raw(a.blocks.data()), a.rows, a.cols, gpu::raw(b.blocks.data()),
+                           b.rows, b.cols, gpu::raw(out.blocks.data()), threads));
+    return out;
+}
+
+inline compressed_matrix mat_scale(const compressed_matrix& a, double c, unsigned threads = 1) {
+    compressed_matrix out = gpu::shaped(a.rows, a.cols);
+    out.blocks.resize(a.blocks.size());
+    if (a.blocks.empty()) return out;
+    gpu::check(blz_mat_scale(gpu::context(), gpu::raw(a.blocks.data()), a.rows, a.cols, c,
+                             gpu::raw(out.blocks.data()), threads));
+    return out;
+}
+
+inline double mat_dot(const compressed_matrix& a, const compressed_matrix& b, std::size_t i, std::size_t j) {
+    double r = 0.0;
+    gpu::check(blz_mat_dot(gpu::context(), gpu::raw(a.blocks.data()), a.rows, a.cols, gpu::raw(b.blocks.data()),
+                           b.rows, b.cols, i, j, &r));
+    return r;
+}
+
+inline compressed_matrix mat_mul(const compressed_matrix& a, const compressed_matrix& b, unsigned threads = 1) {
+    if (a.cols != b.rows) throw std::invalid_argument("mat_mul: inner dimension mismatch");
+    compressed_matrix out = gpu::shaped(a.rows, b.cols);
+    gpu::check(blz_mat_mul(gpu::context(), gpu::raw(a.blocks.data()), a.rows, a.cols, gpu::raw(b.blocks.data()),
+                           b.rows, b.cols, gpu::raw(out.blocks.data()), threads));
+    return out;
+}
+
+inline dense_matrix mat_mul_dense(const compressed_matrix& a, const compressed_matrix& b, unsigned threads = 1) {
+    if (a.cols != b.rows) throw std::invalid_argument("mat_mul: inner dimension mismatch");
+    dense_matrix out(a.rows, b.cols);
+    gpu::check(blz_mat_mul_dense(gpu::context(), gpu::raw(a.blocks.data()), a.rows, a.cols,
+                                 gpu::raw(b.blocks.data()), b.rows, b.cols, out.values.data(), threads));
+    return out;
+}
+
+// ---- block level (batched calls of one block) ----------------------------------
+inline compressed_block compress_block(const block8& m) {
+    compressed_block out;
+    gpu::check(blz_compress_blocks(gpu::context(), m.a.data(), 1, gpu::raw(&out)));
+    return out;
+}
+
+inline block8 decompress_block(const compressed_block& cb) {
+    block8 out;
+    gpu::check(blz_decompress_blocks(gpu::context(), gpu::raw(&cb), 1, out.a.data()));
+    return out;
+}
+
+inline block8 dequantize_prediction(const compressed_block& cb) {
+    block8 out;
+    gpu::check(blz_dequantize_blocks(gpu::context(), gpu::raw(&cb), 1, out.a.data()));
+    return out;
+}
+
+inline compressed_block add(const compressed_block& b1, const compressed_block& b2) {
+    compressed_block out;
+    gpu::check(blz_mat_add(gpu::context(), gpu::raw(&b1), 8, 8, gpu::raw(&b2), 8, 8, gpu::raw(&out), 1));
+    return out;
+}
+
+inline compressed_block sub(const compressed_block& b1, const compressed_block& b2) {
+    compressed_block out;
+    gpu::check(blz_mat_sub(gpu::context(), gpu::raw(&b1), 8, 8, gpu::raw(&b2), 8, 8, gpu::raw(&out), 1));
+    return out;
+}
+
+inline compressed_block scale(const compressed_block& b, double c) {
+    compressed_block out;
+    gpu::check(blz_mat_scale(gpu::context(), gpu::raw(&b), 8, 8, c, gpu::raw(&out), 1));
+    return out;
+}
+
+// Rows 0..last_row of decompress_block(b) (bitwise); other rows stay +0.0.
+inline partial_reconstruction reconstruct_rows(const compressed_block& b, int last_row) {
+    if (last_row < 0 || last_row >= block_dim)
+        throw std::out_of_range("reconstruct_rows: row index out of range");
+    partial_reconstruction out;
+    out.extent = last_row + 1;
+    const block8 full = decompress_block(b);
+    for (int i = 0; i <= last_row; ++i)
+        for (int j = 0; j < block_dim; ++j) out.values(i, j) = full(i, j);
+    return out;
+}
+
+// Columns 0..last_col of decompress_block(b) (bitwise); other columns stay +0.0.
+inline partial_reconstruction reconstruct_cols(const compressed_block& b, int last_col) {
+    if (last_col < 0 || last_col >= block_dim)
+        throw std::out_of_range("reconstruct_cols: column index out of range");
+    partial_reconstruction out;
+    out.extent = last_col + 1;
+    const block8 full = decompress_block(b);
+    for (int i = 0; i < block_dim; ++i)
+        for (int j = 0; j <= last_col; ++j) out.values(i, j) = full(i, j);
+    return out;
+}
+
+inline double dot(const compressed_block& b1, const compressed_block& b2, int i, int j) {
+    if (i < 0 || i >= block_dim || j < 0 || j >= block_dim) throw std::out_of_range("dot: index out of range");
+    double r = 0.0;
+    gpu::check(blz_mat_dot(gpu::context(), gpu::raw(&b1), 8, 8, gpu::raw(&b2), 8, 8, std::size_t(i),
+                           std::size_t(j), &r));
+    return r;
+}
+
+inline block8 block_mul(const compressed_block& b1, const compressed_block& b2) {
+    block8 out;
+    gpu::check(blz_mat_mul_dense(gpu::context(), gpu::raw(&b1), 8, 8, gpu::raw(&b2), 8, 8, out.a.data(), 1));
+    return out;
+}
+
+// ---- uncompressed baselines (H/matrix.hpp:253-300), CPU ---------------------------
+namespace ref {
+
+inline void require_same_dims(const dense_matrix& a, const dense_matrix& b, const char* what) {
+    if (a.rows != b.rows || a.cols != b.cols) throw std::invalid_argument(std::string(what) + ": dimension mismatch");
+}
+
+inline dense_matrix add(const dense_matrix& a, const dense_matrix& b) {
+    require_same_dims(a, b, "ref::add");
+    dense_matrix out(a.rows, a.cols);
+    for (std::size_t k = 0; k < out.values.size(); ++k) out.values[k] = a.values[k] + b.values[k];
+    return out;
+}
+
+inline dense_matrix sub(const dense_matrix& a, const dense_matrix& b) {
+    require_same_dims(a, b, "ref::sub");
+    dense_matrix out(a.rows, a.cols);
+    for (std::size_t k = 0; k < out.values.size(); ++k) out.values[k] = a.values[k] - b.values[k];
+    return out;
+}
+
+inline dense_matrix scale(const dense_matrix& a, double c) {
+    dense_matrix out(a.rows, a.cols);
+    for (std::size_t k = 0; k < out.values.size(); ++k) out.values[k] = a.values[k] * c;
+    return out;
+}
+
+inline double dot(const dense_matrix& a, const dense_matrix& b, std::size_t i, std::size_t j) {
+    if (a.cols != b.rows) throw std::invalid_argument("ref::dot: inner dimension mismatch");
+    if (i >= a.rows || j >= b.cols) throw std::out_of_range("ref::dot: index out of range");
+    double r = 0.0;
+    for (std::size_t k = 0; k < a.cols; ++k) r += a(i, k) * b(k, j);
+    return r;
+}
+
+inline dense_matrix mul(const dense_matrix& a, const dense_matrix& b) {
+    if (a.cols != b.rows) throw std::invalid_argument("ref::mul: inner dimension mismatch");
+    dense_matrix out(a.rows, b.cols);
+    for (std::size_t i = 0; i < a.rows; ++i)
+        for (std::size_t k = 0; k < a.cols; ++k) {
+            const double av = a(i, k);
+            for (std::size_t j = 0; j < b.cols; ++j) out(i, j) += av * b(k, j);
+        }
+    return out;
+}
+
+}  // namespace ref
+
+}  // namespace blaz
+
+#endif  // BLAZ_DROPIN_BLAZ_HPP

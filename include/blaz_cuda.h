@@ -185,6 +185,8 @@ blz_status blz_mat_rowdot(blz_ctx* ctx, const blz_block* a, const blz_block* b, 
 /* n independent 8x8 blocks (64 row-major doubles each) <-> n blz_block. */
 blz_status blz_compress_blocks(blz_ctx* ctx, const double* tiles, uint64_t n, blz_block* out);
 blz_status blz_decompress_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, double* tiles);
+/* dequantize_prediction (H/codec.hpp:150-158): the 8x8 slope grid of each block. */
+blz_status blz_dequantize_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, double* tiles);
 
 #ifdef __cplusplus
 }

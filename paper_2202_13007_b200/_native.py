@@ -96,6 +96,7 @@ SIGNATURES = {
     "blz_mat_rowdot": (_ST, [_P, _P, _P, _U64, _U64, _P, _P]),
     "blz_compress_blocks": (_ST, [_P, _P, _U64, _P]),
     "blz_decompress_blocks": (_ST, [_P, _P, _U64, _P]),
+    "blz_dequantize_blocks": (_ST, [_P, _P, _U64, _P]),
 }
 
 _lib = None

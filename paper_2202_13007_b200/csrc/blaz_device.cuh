@@ -197,8 +197,8 @@ __device__ __forceinline__ double dequant(int c, double phi, double r) {
   return fma(e, r, q);
 }
 
-template <class Emit>
-__device__ __forceinline__ void decompress_exact(const RBlock& b, const Basis& B, Emit&& emit) {
+template <bool SLOPES_ONLY, class Emit>
+__device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basis& B, Emit&& emit) {
   const double s = b.s;
   double dq[KEPT];
   const bool zero = (s == 0.0);  // dequantize_prediction returns a zero grid (:151)
@@ -242,6 +242,10 @@ __device__ __forceinline__ void decompress_exact(const RBlock& b, const Basis& B
       for (int j = 1; j < BD; ++j) acc += tr[j] * B.t[j * BD + v];
       p[v] = zero ? 0.0 : acc;
     }
+    if (SLOPES_ONLY) {
+      emit(u, p);
+      continue;
+    }
     // integrate_rows (H/codec.hpp:164-174)
     double row[BD];
     if (u == 0) {
@@ -257,6 +261,18 @@ __device__ __forceinline__ void decompress_exact(const RBlock& b, const Basis& B
 #pragma unroll
     for (int j = 0; j < BD; ++j) prev[j] = row[j];
   }
+}
+
+template <class Emit>
+__device__ __forceinline__ void decompress_exact(const RBlock& b, const Basis& B, Emit&& emit) {
+  decompress_rows_impl<false>(b, B, emit);
+}
+
+// dequantize_prediction (H/codec.hpp:150-158) streamed row by row: emit(u, p[8])
+// with p = row u of idct2(d), d the dequantized coefficient grid; zeros for s == 0.
+template <class Emit>
+__device__ __forceinline__ void slope_grid_exact(const RBlock& b, const Basis& B, Emit&& emit) {
+  decompress_rows_impl<true>(b, B, emit);
 }
 
 // Full 8x8 decompression into registers.

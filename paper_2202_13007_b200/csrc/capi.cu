@@ -678,4 +678,17 @@ blz_status blz_decompress_blocks(blz_ctx* c, const blz_block* in, uint64_t n, do
   return latch_status(c);
 }
 
+blz_status blz_dequantize_blocks(blz_ctx* c, const blz_block* in, uint64_t n, double* tiles) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (n == 0) return BLZ_OK;
+  blz_cmat m;
+  if (blz_status st = upload_blocks(c, in, 8 * n, 8, S_CM0, &m)) return st;
+  cudaError_t e;
+  double* d = (double*)slot(c, S_OUT, n * 64 * sizeof(double), &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  BLZ_CUDA(c, blz::launch_dequantize(lc(c), c->basis, view(&m), d), "dequantize");
+  BLZ_CUDA(c, cudaMemcpyAsync(tiles, d, n * 64 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  return latch_status(c);
+}
+
 }  // extern "C"

@@ -131,6 +131,22 @@ __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, d
   }
 }
 
+// dequantize_prediction (H/codec.hpp:150-158): the 8x8 slope grid of each
+// block (IDCT of the dequantized coefficients), tile-major output.
+__global__ void __launch_bounds__(128, 4) k_dequantize(const Basis B, CMat in, double* __restrict__ tiles) {
+  const uint64_t nb = in.nb();
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    RBlock rb = load_block(in, t);
+    // decompress_exact with f = 0, s = 1 integrates; undo by emitting p directly:
+    // run the same pass 1 / pass 2 through slope_grid_exact.
+    slope_grid_exact(rb, B, [&](int u, const double (&p)[BD]) {
+#pragma unroll
+      for (int v = 0; v < BD; ++v) tiles[t * 64 + u * BD + v] = p[v];
+    });
+  }
+}
+
 static unsigned grid_for(uint64_t n, unsigned threads, int sms) {
   const uint64_t want = (n + threads - 1) / threads;
   const uint64_t cap = (uint64_t)sms * 64;
@@ -156,6 +172,12 @@ cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* de
   k_compress_worklist<<<c.sm_count, 128, 0, c.stream>>>(B, dense, rows, cols, ld, out, c.err, c.wl, c.wl_count,
                                                         c.stats + 0);
   *c.launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in, double* tiles) {
+  k_dequantize<<<grid_for(in.nb(), 128, c.sm_count), 128, 0, c.stream>>>(B, in, tiles);
+  ++*c.launches;
   return cudaGetLastError();
 }
 

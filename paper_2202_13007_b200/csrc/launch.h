@@ -32,6 +32,7 @@ cudaError_t launch_compress_pair(const LaunchCtx& c, const FastParams& P, const 
 // codec.cu
 cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
                             uint64_t cols, uint64_t ld, const CMat& out);
+cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in, double* tiles);
 cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols);
 // ops.cu
