@@ -127,3 +127,21 @@ def test_oracle_errors(port):
         port.compress_block(bad)
     with pytest.raises(OracleError):
         port.mat_scale(np.zeros(1, port.compress_matrix(np.ones((8, 8))).dtype), float("inf"))
+
+
+def test_markstein_dequant_exhaustive():
+    """C/phi == RN(q + RN? ...) -- the decompress dequantization (blaz_device.cuh::dequant):
+    r = RN(1/phi), q = RN(C*r), e = fma(-phi, q, C), result = fma(e, r, q) equals the IEEE
+    quotient C/phi for every C in [-128, 127] and phi in [1, 255] (fma emulated exactly)."""
+    from fractions import Fraction as F
+    bad = 0
+    for phi in range(1, 256):
+        r = 1.0 / phi
+        fr = F(r)
+        for c in range(-128, 128):
+            q = c * r                                 # DMUL, correctly rounded
+            e = float(F(c) - phi * F(q))              # fma(-phi, q, c): one rounding
+            res = float(F(e) * fr + F(q))             # fma(e, r, q): one rounding
+            if res != c / phi:
+                bad += 1
+    assert bad == 0
