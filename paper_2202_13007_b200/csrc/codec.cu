@@ -4,7 +4,7 @@
 // one thread owns one 8x8 block of the row-major block grid; the per-block
 // arithmetic is blaz_device.cuh.
 #include "blaz_device.cuh"
-#include "fastpath.cuh"
+#include "fastpath.cuh"  // FastParams, NEED_EXACT
 #include "launch.h"
 
 namespace blz {
@@ -55,51 +55,6 @@ __global__ void __launch_bounds__(128) k_compress(const Basis B, const double* _
   }
 }
 
-// Verified fast compress (fastpath.cuh); blocks whose decisions are not
-// certified are appended to the worklist for k_compress_worklist.
-__global__ void __launch_bounds__(128) k_compress_fast(const FastParams P, const double* __restrict__ dense,
-                                                       uint64_t rows, uint64_t cols, uint64_t ld, CMat out,
-                                                       unsigned long long* err, uint64_t* __restrict__ wl,
-                                                       unsigned long long* __restrict__ wl_count) {
-  const uint64_t nb = out.nb();
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t bi = t / out.bc, bj = t % out.bc;
-    double m[BC];
-    load_tile(dense, rows, cols, ld, bi, bj, m);
-    RBlock rb;
-    const uint32_t e = compress_fast(m, P, rb);
-    if (e == NEED_EXACT) {
-      wl[atomicAdd(wl_count, 1ull)] = t;
-      continue;
-    }
-    if (e != DERR_NONE) latch_error(err, t, e);
-    store_block(out, t, rb);
-  }
-}
-
-// Exact compress of the listed blocks (the certified-slow path).
-__global__ void __launch_bounds__(128) k_compress_worklist(const Basis B, const double* __restrict__ dense,
-                                                           uint64_t rows, uint64_t cols, uint64_t ld, CMat out,
-                                                           unsigned long long* err,
-                                                           const uint64_t* __restrict__ wl,
-                                                           const unsigned long long* __restrict__ wl_count,
-                                                           unsigned long long* stats) {
-  const uint64_t n = *wl_count;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(stats, (unsigned long long)n);
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
-       q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t t = wl[q];
-    const uint64_t bi = t / out.bc, bj = t % out.bc;
-    double m[BC];
-    load_tile(dense, rows, cols, ld, bi, bj, m);
-    RBlock rb;
-    const uint32_t e = compress_exact(m, B, rb);
-    if (e != DERR_NONE) latch_error(err, t, e);
-    store_block(out, t, rb);
-  }
-}
-
 // Warp-uniform loop (valid lanes predicated) so that the basis streams through
 // uniform registers (LDCU.128) rather than per-thread constant loads.
 __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, double* __restrict__ dense,
@@ -133,7 +88,7 @@ __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, d
 
 // dequantize_prediction (H/codec.hpp:150-158): the 8x8 slope grid of each
 // block (IDCT of the dequantized coefficients), tile-major output.
-__global__ void __launch_bounds__(128, 4) k_dequantize(const Basis B, CMat in, double* __restrict__ tiles) {
+__global__ void __launch_bounds__(128) k_dequantize(const Basis B, CMat in, double* __restrict__ tiles) {
   const uint64_t nb = in.nb();
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nb;
        t += (uint64_t)gridDim.x * blockDim.x) {
@@ -169,9 +124,7 @@ cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* de
   P.zero = 0;
   e = launch_compress_pair(c, P, dense, rows, cols, ld, out);
   if (e != cudaSuccess) return e;
-  k_compress_worklist<<<c.sm_count, 128, 0, c.stream>>>(B, dense, rows, cols, ld, out, c.err, c.wl, c.wl_count,
-                                                        c.stats + 0);
-  *c.launches += 1;
+  e = launch_compress_worklist_warp(c, B, dense, rows, cols, ld, out);
   return cudaGetLastError();
 }
 

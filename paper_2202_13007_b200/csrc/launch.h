@@ -29,6 +29,9 @@ struct LaunchCtx {
 struct FastParams;
 cudaError_t launch_compress_pair(const LaunchCtx& c, const FastParams& P, const double* dense, uint64_t rows,
                                  uint64_t cols, uint64_t ld, const CMat& out);
+// compress_exact_warp.cu (exact compress of the worklist, one warp per block)
+cudaError_t launch_compress_worklist_warp(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
+                                          uint64_t cols, uint64_t ld, const CMat& out);
 // codec.cu
 cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
                             uint64_t cols, uint64_t ld, const CMat& out);
