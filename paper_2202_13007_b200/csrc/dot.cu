@@ -56,28 +56,71 @@ __global__ void __launch_bounds__(128) k_dot_entries(const Basis B, CMat a, CMat
   }
 }
 
-// One thread per block-row: 8 running row sums, blocks ascending.
-__global__ void __launch_bounds__(128) k_rowdot(const Basis B, CMat a, CMat b, double* __restrict__ r) {
-  for (uint64_t bi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; bi < a.br;
-       bi += (uint64_t)gridDim.x * blockDim.x) {
-    double acc[BD];
+// Row dots r_i = sum_j Ahat(i,j) Bhat(i,j), ascending j from +0.0.
+// A warp covers 4 block-rows.  Per chunk of 4 block-columns, lanes 0-15
+// decompress the 16 A blocks and lanes 16-31 the 16 matching B blocks (exact,
+// one decompression per lane) into shared memory; then lane L advances the
+// serial chain of row (L & 7) of block-row (L >> 3) over the chunk's 4 blocks
+// x 8 columns in ascending order: acc += a*b (DMUL then DADD) -- the identical
+// operation sequence as the single-threaded restatement.  Row stride 9 and
+// slot stride 74 doubles keep the chain reads bank-conflict-free.
+constexpr int RD_WARPS = 2;
+constexpr int RD_SLOT = 74;
+
+__global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a, CMat b, double* __restrict__ r) {
+  __shared__ double P[RD_WARPS][32 * RD_SLOT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* S = P[warp];
+  const uint64_t groups = (a.br + 3) / 4;
+  // decompression role of this lane
+  const bool is_b = lane >= 16;
+  const int dl = lane & 15;
+  const int dgrp = dl >> 2, dcol = dl & 3;
+  // chain role of this lane
+  const int cgrp = lane >> 3, u_own = lane & 7;
+  for (uint64_t g = blockIdx.x * (uint64_t)RD_WARPS + warp; g < groups; g += (uint64_t)gridDim.x * RD_WARPS) {
+    const uint64_t drow = g * 4 + dgrp, crow = g * 4 + cgrp;
+    double acc = 0.0;
+    for (uint64_t t0 = 0; t0 < a.bc; t0 += 4) {
+      // no divergent branch around the decompression (keeps the basis in
+      // uniform registers): out-of-range lanes decompress a clamped block
+      // into their own slot, which the chain phase never reads
+      {
+        const uint64_t t = min(t0 + dcol, a.bc - 1), dr = min(drow, a.br - 1);
+        const uint64_t idx = dr * a.bc + t;
+        RBlock blk;
+        blk.f = is_b ? b.first[idx] : a.first[idx];
+        blk.s = is_b ? b.slope[idx] : a.slope[idx];
+        blk.phi = is_b ? b.scale[idx] : a.scale[idx];
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>((is_b ? b.coeffs : a.coeffs) + idx * KEPT);
 #pragma unroll
-    for (int i = 0; i < BD; ++i) acc[i] = 0.0;
-    for (uint64_t t = 0; t < a.bc; ++t) {
-      double da[BC];
-      decompress_exact_full(load_block(a, bi * a.bc + t), B, da);
-      const RBlock bb = load_block(b, bi * b.bc + t);
-      const uint64_t rem = a.cols - t * BD;
-      const int jlim = rem < BD ? (int)rem : BD;
-      decompress_exact(bb, B, [&](int u, const double (&row)[BD]) {
+        for (int w = 0; w < 7; ++w) blk.c[w] = cw[w];
+        double* slot = S + lane * RD_SLOT;
+        decompress_exact(blk, B, [&](int u, const double (&row)[BD]) {
 #pragma unroll
-        for (int j = 0; j < BD; ++j)
-          if (j < jlim) acc[u] += da[u * BD + j] * row[j];
-      });
+          for (int v = 0; v < BD; ++v) slot[u * 9 + v] = row[v];
+        });
+      }
+      __syncwarp();
+      if (crow < a.br) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t tk = t0 + k;
+          if (tk < a.bc) {
+            const uint64_t rem = a.cols - tk * BD;
+            const int jlim = rem < BD ? (int)rem : BD;
+            const double* sa = S + (cgrp * 4 + k) * RD_SLOT + u_own * 9;
+            const double* sb = S + (16 + cgrp * 4 + k) * RD_SLOT + u_own * 9;
+#pragma unroll
+            for (int v = 0; v < BD; ++v)
+              if (v < jlim) acc += sa[v] * sb[v];
+          }
+        }
+      }
+      __syncwarp();
     }
-#pragma unroll
-    for (int i = 0; i < BD; ++i)
-      if (bi * BD + i < a.rows) r[bi * BD + i] = acc[i];
+    const uint64_t row = crow * BD + u_own;
+    if (crow < a.br && row < a.rows) r[row] = acc;
   }
 }
 
@@ -100,8 +143,11 @@ cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a
 }
 
 cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r) {
-  const unsigned g = (unsigned)((a.br + 127) / 128);
-  k_rowdot<<<g ? g : 1, 128, 0, c.stream>>>(B, a, b, r);
+  const uint64_t groups = (a.br + 3) / 4;
+  const uint64_t want = (groups + RD_WARPS - 1) / RD_WARPS;
+  const uint64_t cap = (uint64_t)c.sm_count * 16;
+  const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+  k_rowdot<<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r);
   ++*c.launches;
   return cudaGetLastError();
 }

@@ -237,3 +237,26 @@ def test_fast_path_cfg1_sample(port):
     used_exact = ctx.stats()["compress_exact_blocks"] - before
     assert blocks_equal(ca.to_host().blocks, port.compress_matrix(a.numpy()))
     assert used_exact <= 0.001 * ca.nblocks, used_exact
+
+
+def test_rowdot_frobenius_medium(port):
+    """Config-2 restatement at a CPU-checkable size (512 x 4100, ragged columns)."""
+    a = W.smooth_field(512, 4100, seed=31).numpy()
+    b = W.smooth_field(512, 4100, seed=32).numpy()
+    A, B = dev.compress(torch.from_numpy(a).cuda()), dev.compress(torch.from_numpy(b).cuda())
+    r, tot = dev.frobenius(A, B)
+    oa, ob = A.to_host().blocks, B.to_host().blocks
+    want = port.rowdot(oa, ob, 512, 4100)
+    assert np.array_equal(bits(r.cpu().numpy()), bits(want))
+    assert np.float64(tot.item()).view(np.uint64) == np.float64(port.sum_ascending(want)).view(np.uint64)
+
+
+def test_rowdot_block_row_tail(port):
+    """Block-row count not a multiple of 4 and a single block column."""
+    for rows, cols in [(40, 8), (13, 3), (72, 70)]:
+        a = W.smooth_field(rows, cols, seed=rows).numpy()
+        b = W.quadratic_blocks(rows, cols, seed=cols).numpy()
+        A, B = dev.compress(torch.from_numpy(a).cuda()), dev.compress(torch.from_numpy(b).cuda())
+        r = dev.rowdot(A, B).cpu().numpy()
+        want = port.rowdot(A.to_host().blocks, B.to_host().blocks, rows, cols)
+        assert np.array_equal(bits(r), bits(want)), (rows, cols)

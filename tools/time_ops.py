@@ -28,7 +28,8 @@ out = torch.empty_like(A)
 dev.compress(A, cA)
 dev.compress(B, cB)
 fns = {"compress": lambda: dev.compress(A, cA), "decompress": lambda: dev.decompress(cA, out),
-       "add": lambda: dev.add(cA, cB, cS), "sub": lambda: dev.sub(cA, cB, cS), "scale": lambda: dev.scale(cA, 3.5, cS)}
+       "add": lambda: dev.add(cA, cB, cS), "sub": lambda: dev.sub(cA, cB, cS), "scale": lambda: dev.scale(cA, 3.5, cS),
+       "rowdot": lambda: dev.rowdot(cA, cB), "frobenius": lambda: dev.frobenius(cA, cB)}
 res = {}
 for name in args.ops.split(","):
     f = fns[name]
