@@ -3,77 +3,248 @@
 // mat_mul_impl (H/matrix.hpp:204-217) accumulates every output entry as
 // acc = 0.0; acc += a(i,k) * b(k,j) over the global inner index k ascending
 // (accumulate_product_tile, :188-202), padding excluded (k < a.cols).
-// Exact mode keeps that order with DMUL+DADD (this TU is built with
-// -fmad=false); fused mode uses DFMA in the same order (tolerance parity).
+//
+//  * BLZ_GEMM_EXACT -- k_gemm_exact: CUDA-core DMUL + DADD (this TU is built
+//    with -fmad=false) in exactly that order: bitwise equal to the reference.
+//    Tiles beyond K are zero-filled: adding +0.0 to a running sum that starts
+//    at +0.0 (and is therefore never -0.0) is the identity.
+//  * BLZ_GEMM_FUSED -- k_gemm_dmma: FP64 tensor cores (mma.sync m8n8k4 f64,
+//    DMMA).  On B200 one DMMA equals the ascending-k chain of fused
+//    multiply-adds (tools/microbench/dmma_semantics.cu: 0 mismatches in 1.28M
+//    entries), so the result is acc = fma(a(i,k), b(k,j), acc), k ascending,
+//    from +0.0: deterministic, tolerance parity against the exact product.
+#include <cuda_pipeline_primitives.h>
+
 #include "launch.h"
 
 namespace blz {
 
-constexpr int GBM = 64, GBN = 64, GBK = 16, GTM = 4, GTN = 4;
+// ---------------------------------------------------------------------------
+// exact SIMT DGEMM: 128x128 CTA tile, BK = 8, 256 threads, 8x8 per thread
+// ---------------------------------------------------------------------------
+constexpr int EBM = 128, EBN = 128, EBK = 8;
+constexpr int EAS = EBK + 1;  // A tile row stride (padded): As[m][k]
 
-template <bool FUSED>
-__global__ void __launch_bounds__(256) k_gemm(const double* __restrict__ A, uint64_t lda,
-                                              const double* __restrict__ Bm, uint64_t ldb,
-                                              double* __restrict__ Cm, uint64_t ldc, uint64_t M,
-                                              uint64_t N, uint64_t K) {
-  __shared__ double As[GBK][GBM + 1];
-  __shared__ double Bs[GBK][GBN];
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const uint64_t m0 = (uint64_t)blockIdx.y * GBM, n0 = (uint64_t)blockIdx.x * GBN;
-  double acc[GTM][GTN];
-#pragma unroll
-  for (int i = 0; i < GTM; ++i)
-#pragma unroll
-    for (int j = 0; j < GTN; ++j) acc[i][j] = 0.0;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  __pipeline_memcpy_async(smem, gmem, 16);
+}
 
-  for (uint64_t k0 = 0; k0 < K; k0 += GBK) {
-    // A tile: GBM x GBK (transposed into smem), B tile: GBK x GBN
-    for (int e = threadIdx.x; e < GBM * GBK; e += 256) {
-      const int r = e / GBK, kk = e % GBK;
-      const uint64_t gr = m0 + r, gk = k0 + kk;
-      As[kk][r] = (gr < M && gk < K) ? A[gr * lda + gk] : 0.0;
+__global__ void __launch_bounds__(256) k_gemm_exact(const double* __restrict__ A, uint64_t lda,
+                                                    const double* __restrict__ Bm, uint64_t ldb,
+                                                    double* __restrict__ Cm, uint64_t ldc, uint64_t M,
+                                                    uint64_t N, uint64_t K) {
+  __shared__ __align__(16) double As[2][EBM * EAS];
+  __shared__ __align__(16) double Bs[2][EBK * EBN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const uint64_t m0 = (uint64_t)blockIdx.y * EBM, n0 = (uint64_t)blockIdx.x * EBN;
+  const bool vecA = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  const bool vecB = ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(Bm) & 15) == 0);
+
+  auto load_tile = [&](int buf, uint64_t k0) {
+    // A: 128 rows x 8 k = 512 double2 chunks -> 2 per thread
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + r * 256;
+      const int row = e >> 2, kc = (e & 3) * 2;
+      const uint64_t gr = m0 + row, gk = k0 + kc;
+      double* dst = &As[buf][row * EAS + kc];
+      if (gr < M && gk + 1 < K && vecA) {
+        const double2 v = *reinterpret_cast<const double2*>(A + gr * lda + gk);  // 8-byte aligned rows (EAS odd)
+        dst[0] = v.x;
+        dst[1] = v.y;
+      } else {
+        dst[0] = (gr < M && gk < K) ? A[gr * lda + gk] : 0.0;
+        dst[1] = (gr < M && gk + 1 < K) ? A[gr * lda + gk + 1] : 0.0;
+      }
     }
-    for (int e = threadIdx.x; e < GBK * GBN; e += 256) {
-      const int kk = e / GBN, cc = e % GBN;
-      const uint64_t gk = k0 + kk, gc = n0 + cc;
-      Bs[kk][cc] = (gk < K && gc < N) ? Bm[gk * ldb + gc] : 0.0;
+    // B: 8 rows x 128 cols = 512 double2 chunks -> 2 per thread (cp.async)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + r * 256;
+      const int kr = e >> 6, cc = (e & 63) * 2;
+      const uint64_t gk = k0 + kr, gc = n0 + cc;
+      double* dst = &Bs[buf][kr * EBN + cc];
+      if (gk < K && gc + 1 < N && vecB) {
+        cp_async16(dst, Bm + gk * ldb + gc);
+      } else {
+        dst[0] = (gk < K && gc < N) ? Bm[gk * ldb + gc] : 0.0;
+        dst[1] = (gk < K && gc + 1 < N) ? Bm[gk * ldb + gc + 1] : 0.0;
+      }
+    }
+    __pipeline_commit();
+  };
+
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+
+  const uint64_t ntiles = (K + EBK - 1) / EBK;
+  load_tile(0, 0);
+  for (uint64_t kt = 0; kt < ntiles; ++kt) {
+    const int buf = (int)(kt & 1);
+    if (kt + 1 < ntiles) {
+      load_tile(buf ^ 1, (kt + 1) * EBK);
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
     }
     __syncthreads();
-    const int kmax = (K - k0) < (uint64_t)GBK ? (int)(K - k0) : GBK;
-    for (int kk = 0; kk < kmax; ++kk) {
-      double av[GTM], bv[GTN];
 #pragma unroll
-      for (int i = 0; i < GTM; ++i) av[i] = As[kk][ty * GTM + i];
+    for (int kk = 0; kk < EBK; ++kk) {
+      double av[8], bv[8];
 #pragma unroll
-      for (int j = 0; j < GTN; ++j) bv[j] = Bs[kk][tx * GTN + j];
+      for (int i = 0; i < 8; ++i) av[i] = As[buf][(ty * 8 + i) * EAS + kk];
+      // thread columns: (j/2)*32 + 2*tx + (j%2) -- 8 lanes read 128 contiguous bytes
 #pragma unroll
-      for (int i = 0; i < GTM; ++i)
+      for (int j = 0; j < 8; j += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk * EBN + (j / 2) * 32 + 2 * tx]);
+        bv[j] = v.x;
+        bv[j + 1] = v.y;
+      }
 #pragma unroll
-        for (int j = 0; j < GTN; ++j) {
-          if (FUSED)
-            acc[i][j] = __fma_rn(av[i], bv[j], acc[i][j]);
-          else
-            acc[i][j] = acc[i][j] + av[i] * bv[j];
-        }
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = acc[i][j] + av[i] * bv[j];
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < GTM; ++i)
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t gr = m0 + ty * 8 + i;
+    if (gr >= M) continue;
 #pragma unroll
-    for (int j = 0; j < GTN; ++j) {
-      const uint64_t gr = m0 + ty * GTM + i, gc = n0 + tx * GTN + j;
-      if (gr < M && gc < N) Cm[gr * ldc + gc] = acc[i][j];
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t gc = n0 + (j / 2) * 32 + 2 * tx + (j % 2);
+      if (gc < N) Cm[gr * ldc + gc] = acc[i][j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused DGEMM on FP64 tensor cores (DMMA m8n8k4), ascending k
+// CTA tile 128x128, BK = 16, 8 warps (each 64 x 32: 8 x 4 MMA tiles)
+// ---------------------------------------------------------------------------
+constexpr int DBM = 128, DBN = 128, DBK = 16;
+constexpr int DAS = DBK + 4;   // As[m][k] row stride = 4 mod 16 doubles: conflict-free fragment loads
+constexpr int DBS = DBN + 4;   // Bs[k][n] row stride = 4 mod 16 doubles
+
+__global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A, uint64_t lda,
+                                                   const double* __restrict__ Bm, uint64_t ldb,
+                                                   double* __restrict__ Cm, uint64_t ldc, uint64_t M,
+                                                   uint64_t N, uint64_t K) {
+  extern __shared__ __align__(16) double dsm[];
+  double* As0 = dsm;
+  double* Bs0 = dsm + 2 * DBM * DAS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps: 64 rows x 32 cols each
+  const uint64_t m0 = (uint64_t)blockIdx.y * DBM, n0 = (uint64_t)blockIdx.x * DBN;
+
+  const bool vecA = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  const bool vecB = ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(Bm) & 15) == 0);
+  auto load_tile = [&](int buf, uint64_t k0) {
+    double* As = As0 + buf * DBM * DAS;
+    double* Bs = Bs0 + buf * DBK * DBS;
+    // A: 128 x 16 = 1024 16-byte chunks -> 4 per thread
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + r * 256;
+      const int row = e >> 3, kc = (e & 7) * 2;
+      const uint64_t gr = m0 + row, gk = k0 + kc;
+      double* dst = As + row * DAS + kc;
+      if (vecA && gr < M && gk + 1 < K) {
+        cp_async16(dst, A + gr * lda + gk);
+      } else {
+        dst[0] = (gr < M && gk < K) ? A[gr * lda + gk] : 0.0;
+        dst[1] = (gr < M && gk + 1 < K) ? A[gr * lda + gk + 1] : 0.0;
+      }
+    }
+    // B: 16 x 128 = 1024 16-byte chunks -> 4 per thread
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + r * 256;
+      const int kr = e >> 6, cc = (e & 63) * 2;
+      const uint64_t gk = k0 + kr, gc = n0 + cc;
+      double* dst = Bs + kr * DBS + cc;
+      if (vecB && gk < K && gc + 1 < N) {
+        cp_async16(dst, Bm + gk * ldb + gc);
+      } else {
+        dst[0] = (gk < K && gc < N) ? Bm[gk * ldb + gc] : 0.0;
+        dst[1] = (gk < K && gc + 1 < N) ? Bm[gk * ldb + gc + 1] : 0.0;
+      }
+    }
+    __pipeline_commit();
+  };
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const uint64_t ntiles = (K + DBK - 1) / DBK;
+  load_tile(0, 0);
+  for (uint64_t kt = 0; kt < ntiles; ++kt) {
+    const int buf = (int)(kt & 1);
+    if (kt + 1 < ntiles) {
+      load_tile(buf ^ 1, (kt + 1) * DBK);
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
+    }
+    __syncthreads();
+    const double* As = As0 + buf * DBM * DAS;
+    const double* Bs = Bs0 + buf * DBK * DBS;
+#pragma unroll
+    for (int ks = 0; ks < DBK; ks += 4) {
+      double fa[8], fb[4];
+      // A fragment (8x4, row): row = lane>>2, col = lane&3
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fa[i] = As[(wm * 64 + i * 8 + (lane >> 2)) * DAS + ks + (lane & 3)];
+      // B fragment (4x8, col): row = lane&3, col = lane>>2
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = Bs[(ks + (lane & 3)) * DBS + wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(fa[i]), "d"(fb[j]));
+    }
+    __syncthreads();
+  }
+  // D fragment: row = lane>>2, cols = (lane&3)*2 + {0,1}
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t gr = m0 + wm * 64 + i * 8 + (lane >> 2);
+      const uint64_t gc = n0 + wn * 32 + j * 8 + (lane & 3) * 2;
+      if (gr < M) {
+        if (gc < N) Cm[gr * ldc + gc] = acc[i][j][0];
+        if (gc + 1 < N) Cm[gr * ldc + gc + 1] = acc[i][j][1];
+      }
     }
 }
 
 cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t lda, const double* Bm,
                         uint64_t ldb, double* Cm, uint64_t ldc, uint64_t M, uint64_t N, uint64_t K) {
-  dim3 grid((unsigned)((N + GBN - 1) / GBN), (unsigned)((M + GBM - 1) / GBM));
-  if (mode == 1)
-    k_gemm<true><<<grid, 256, 0, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
-  else
-    k_gemm<false><<<grid, 256, 0, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
+  if (mode == 1) {
+    dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
+    const size_t smem = (size_t)(2 * DBM * DAS + 2 * DBK * DBS) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_gemm_dmma<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
+  } else {
+    dim3 grid((unsigned)((N + EBN - 1) / EBN), (unsigned)((M + EBM - 1) / EBM));
+    k_gemm_exact<<<grid, 256, 0, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
+  }
   ++*c.launches;
   return cudaGetLastError();
 }

@@ -260,3 +260,30 @@ def test_rowdot_block_row_tail(port):
         r = dev.rowdot(A, B).cpu().numpy()
         want = port.rowdot(A.to_host().blocks, B.to_host().blocks, rows, cols)
         assert np.array_equal(bits(r), bits(want)), (rows, cols)
+
+
+def test_matmul_exact_medium(port):
+    """Exact compressed GEMM (SIMT DMUL+DADD, ascending k) vs the oracle, ragged sizes
+    spanning several 128 x 128 CTA tiles and a K not a multiple of the k-tile."""
+    a = W.smooth_field(264, 333, seed=41).numpy()
+    b = W.quadratic_blocks(333, 200, seed=42).numpy()
+    A, B = dev.compress(torch.from_numpy(a).cuda()), dev.compress(torch.from_numpy(b).cuda())
+    oa, ob = A.to_host().blocks, B.to_host().blocks
+    got = dev.matmul_dense(A, B, mode=blz.GEMM_EXACT).cpu().numpy()
+    want = port.mat_mul_dense(oa, 264, 333, ob, 333, 200)
+    assert np.array_equal(bits(got), bits(want))
+    gc = dev.matmul(A, B, mode=blz.GEMM_EXACT).to_host().blocks
+    wc = port.mat_mul(oa, 264, 333, ob, 333, 200)
+    assert blocks_equal(gc, wc), block_diff_report(gc, wc)
+
+
+def test_matmul_fused_dmma_tolerance(port):
+    """Fused mode = DMMA tensor cores (ascending-k FMA chain): normwise tolerance vs exact."""
+    a = W.smooth_field(256, 512, seed=43).numpy()
+    b = W.smooth_field(512, 256, seed=44).numpy()
+    A, B = dev.compress(torch.from_numpy(a).cuda()), dev.compress(torch.from_numpy(b).cuda())
+    exact = dev.matmul_dense(A, B, mode=blz.GEMM_EXACT).cpu().numpy()
+    fused = dev.matmul_dense(A, B, mode=blz.GEMM_FUSED).cpu().numpy()
+    err = np.max(np.abs(fused - exact)) / max(1.0, np.max(np.abs(exact)))
+    assert err <= 1e-13 * 512, err
+    assert np.array_equal(bits(fused), bits(dev.matmul_dense(A, B, mode=blz.GEMM_FUSED).cpu().numpy()))  # deterministic

@@ -30,7 +30,12 @@ dev.compress(B, cB)
 fns = {"compress": lambda: dev.compress(A, cA), "decompress": lambda: dev.decompress(cA, out),
        "add": lambda: dev.add(cA, cB, cS), "sub": lambda: dev.sub(cA, cB, cS), "scale": lambda: dev.scale(cA, 3.5, cS),
        "rowdot": lambda: dev.rowdot(cA, cB), "frobenius": lambda: dev.frobenius(cA, cB)}
+if any(o.startswith("matmul") for o in args.ops.split(",")):
+    scratch = dev.matmul_scratch(cA, cB)
+    fns["matmul_exact"] = lambda: dev.matmul(cA, cB, mode=0, out=cS, scratch=scratch)
+    fns["matmul_fused"] = lambda: dev.matmul(cA, cB, mode=1, out=cS, scratch=scratch)
 res = {}
+flops = {"matmul_exact": 2.0 * rows ** 3, "matmul_fused": 2.0 * rows ** 3}
 for name in args.ops.split(","):
     f = fns[name]
     for _ in range(3):
@@ -43,5 +48,7 @@ for name in args.ops.split(","):
     e1.record()
     torch.cuda.synchronize()
     res[name] = round(e0.elapsed_time(e1) / args.reps, 4)
+    if name in flops:
+        res[name + "_tflops"] = round(flops[name] / (res[name] * 1e-3) / 1e12, 2)
 dev.sync()
 print(json.dumps({"lib": os.environ.get("BLZ_LIB_PATH", "in-tree"), "ms": res}))
