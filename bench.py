@@ -306,7 +306,7 @@ def run_ours(args, cfg, rank, world, local):
             "config": {"workload": args.config, "rows": rows, "cols": cols, "blocks_per_matrix": nb,
                        "parallelism": f"block-row shards x{world} (no collective)",
                        "l2": "inputs larger than L2 (2 GiB dense operands, 189 MB compressed)",
-                       "mode": "exact (-fmad=false, reference order)"},
+                       "mode": "bit-exact: verified fast compress + reference-order kernels (-fmad=false)"},
             "ops": op_report,
             "roofline": {"bound": "hbm", "kernel": "k_decompress", "achieved": dec["gbs"], "peak": hbm,
                          "peak_kind": hbm_kind, "unit": "GB/s", "frac": dec["hbm_frac"],
@@ -314,12 +314,171 @@ def run_ours(args, cfg, rank, world, local):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "parity": parity,
+            "compress_exact_path_blocks": ctx.stats()["compress_exact_blocks"],
         }
         if e2e is not None:
             line["e2e"] = e2e
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(args, cfg)
+    del A, B, cA, cB, cS, cD, cK, oS, oD, oK
+    torch.cuda.empty_cache()
+    if not args.no_extras and world == 1:
+        extras = run_extras(args)
+        if line is not None:
+            line["configs"] = extras
     return line
+
+
+def _chunked_compress(gen, rows, cols, seed, chunk_rows=8192):
+    """Compresses a rows x cols matrix generated chunk by chunk (bounded memory);
+    returns the DeviceCMat and the dense rows of chunk 0 (for parity sampling)."""
+    import torch
+
+    from paper_2202_13007_b200 import device as dev
+    from paper_2202_13007_b200 import workloads as W
+    full = dev.DeviceCMat(rows, cols)
+    bc = (cols + 7) // 8
+    first_rows = None
+    for r0 in range(0, rows, chunk_rows):
+        nr = min(chunk_rows, rows - r0)
+        if gen == "smooth":
+            d = W.smooth_field(nr, cols, seed, device="cuda", row0=r0)
+        else:
+            d = W.make(gen, nr, cols, seed + r0, device="cuda")
+        part = dev.compress(d)
+        b0, b1 = (r0 // 8) * bc, (r0 // 8) * bc + part.nblocks
+        full.first[b0:b1].copy_(part.first)
+        full.slope[b0:b1].copy_(part.slope)
+        full.coeffs[b0:b1].copy_(part.coeffs)
+        full.scale[b0:b1].copy_(part.scale)
+        if r0 == 0:
+            first_rows = d[:64].cpu().numpy()
+        del d, part
+    torch.cuda.synchronize()
+    return full, first_rows
+
+
+def _time(fn, reps, warm=1):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def run_extras(args):
+    """Configs 2 and 3 of BASELINE.json on one GPU (reported beside the cfg1 headline)."""
+    import numpy as np
+    import torch
+
+    from paper_2202_13007_b200 import device as dev
+    out = {}
+    fp64_peak = 36.6  # TFLOP/s, DMMA/DFMA measured (profiles/r01_fp64_peaks.txt)
+    # ---- config 2: row dots + Frobenius of two 65536^2 smooth fields -------------------
+    n2 = args.cfg2_size
+    A, a_rows = _chunked_compress("smooth", n2, n2, 11)
+    B, b_rows = _chunked_compress("smooth", n2, n2, 12)
+    r_holder = {}
+
+    def frob():
+        r_holder["r"], r_holder["t"] = dev.frobenius(A, B)
+    ms = _time(frob, reps=args.extra_reps)
+    nb2 = A.nblocks
+    rec = {"workload": f"cfg2 rowdot+frobenius {n2}x{n2} (smooth fields)", "ms": round(ms, 3),
+           "value": nb2 / (ms * 1e-3), "unit": "block pairs/s",
+           "fp64_note": "exact: two reference-order decompressions per block pair (~3.4k FP64 ops) + serial row chains"}
+    if not args.no_parity:
+        from oracle import oracle as O
+        port = O.port()
+        bc = (n2 + 7) // 8
+        ha, hb = A.to_host(), B.to_host()
+        want = port.rowdot(ha.blocks[:8], hb.blocks[:8], 64, n2)
+        got = r_holder["r"][:64].cpu().numpy()
+        rec["parity"] = {"sampled_rows": 64, "bit_exact": bool(np.array_equal(got.view(np.uint64), want.view(np.uint64)))}
+        del ha, hb
+    if not args.no_cpu_baseline:
+        rec["cpu_baseline"] = cpu_baseline_rowdot(a_rows, b_rows, n2)
+    out["cfg2"] = rec
+    del A, B, r_holder
+    torch.cuda.empty_cache()
+    # ---- config 3: compressed matmul 8192^3 ------------------------------------------------
+    n3 = args.cfg3_size
+    A, a_rows = _chunked_compress("smooth", n3, n3, 21)
+    B, _ = _chunked_compress("smooth", n3, n3, 22)
+    C = dev.DeviceCMat(n3, n3)
+    scratch = dev.matmul_scratch(A, B)
+    flops = 2.0 * n3 ** 3
+    rec = {"workload": f"cfg3 compressed matmul {n3}^3 (compressed in, compressed out)"}
+    for mode, name in ((0, "exact"), (1, "fused_dmma")):
+        ms = _time(lambda: dev.matmul(A, B, mode=mode, out=C, scratch=scratch), reps=args.extra_reps)
+        tf = flops / (ms * 1e-3) / 1e12
+        rec[name] = {"ms": round(ms, 3), "tflops": round(tf, 2), "frac_fp64_peak": round(tf / fp64_peak, 3)}
+    rec["exact"]["note"] = "DMUL+DADD in the reference's order: capped at 50% of the FP64 FMA peak"
+    rec["fused_dmma"]["note"] = "FP64 tensor cores; = ascending-k FMA chain; tolerance parity"
+    if not args.no_parity:
+        from oracle import oracle as O
+        port = O.port()
+        dev.matmul(A, B, mode=0, out=C, scratch=scratch)
+        # row block 0 of C vs the oracle (A's first block-row against all of B)
+        ha, hb = A.to_host(), B.to_host()
+        want = port.mat_mul(ha.blocks[:1], 8, n3, hb.blocks, n3, n3)
+        hc = C.to_host().blocks[:1]
+        same = all(np.array_equal(np.ascontiguousarray(hc[f]).view(np.uint8), np.ascontiguousarray(want[f]).view(np.uint8))
+                   for f in ("first", "slope", "scale_factor", "coeffs"))
+        rec["parity"] = {"sampled_block_rows": 1, "exact_mode_bit_exact": bool(same)}
+        del ha, hb
+    if not args.no_cpu_baseline:
+        rec["cpu_baseline"] = cpu_baseline_matmul(a_rows, n3)
+    out["cfg3"] = rec
+    del A, B, C, scratch
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_baseline_rowdot(a_rows, b_rows, n):
+    """Reference decompress_matrix (all host threads) + ascending row sums on a 64-row slice."""
+    import numpy as np
+
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None
+    r = O.ref()
+    threads = host_threads()
+    ca = r.compress_matrix(a_rows, threads)
+    cb = r.compress_matrix(b_rows, threads)
+    t0 = time.perf_counter()
+    da = r.decompress_matrix(ca, 64, n, threads)
+    db = r.decompress_matrix(cb, 64, n, threads)
+    _ = np.einsum("ij,ij->i", da, db)
+    dt = time.perf_counter() - t0
+    pairs = 8 * ((n + 7) // 8)
+    return {"value": pairs / dt, "unit": "block pairs/s", "cores": threads, "kind": "reference",
+            "sample": f"64 x {n} slice: reference decompress_matrix of A and B + row sums"}
+
+
+def cpu_baseline_matmul(a_rows, n):
+    """Reference mat_mul of an 8-row slice of A by the full B (all host threads)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None
+    import paper_2202_13007_b200.workloads as W
+    r = O.ref()
+    threads = host_threads()
+    b = W.smooth_field(n, n, 22).numpy()
+    ca = r.compress_matrix(a_rows[:8], threads)
+    cb = r.compress_matrix(b, threads)
+    t0 = time.perf_counter()
+    r.mat_mul(ca, 8, n, cb, n, n, threads)
+    dt = time.perf_counter() - t0
+    flops = 2.0 * 8 * n * n
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+            "sample": f"8 x {n} by {n} x {n}: reference mat_mul (includes decompressing all of B)"}
 
 
 def load_traffic(kernel):
@@ -442,6 +601,10 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--ref-sample-rows", type=int, default=512)
     ap.add_argument("--cpu-repeats", type=int, default=3)
+    ap.add_argument("--no-extras", action="store_true", help="skip the config-2/3 measurements")
+    ap.add_argument("--cfg2-size", type=int, default=65536)
+    ap.add_argument("--cfg3-size", type=int, default=8192)
+    ap.add_argument("--extra-reps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     cfg = CONFIGS[args.config]
