@@ -47,16 +47,25 @@ struct PairShared {
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 // Certified decision on y (see fastpath.cuh::decide): t = y + 1.5*2^20 + 0.5
-// puts floor(y + 0.5) + 2^19 in the low 20 bits of the high word and the
-// fraction in the low word.  A signed max of the high word with 0x41300000
-// maps every out-of-range y (|y| >= 2^19, negative t, NaN) onto |n| >= 2^19,
-// which the callers' clamps send to the correct end of their range.
-__device__ __forceinline__ int decide_n(double y, uint32_t& dist) {
+// lies in [2^20, 2^21) for |y| < 2^19, where its high word is
+// 0x41380000 + floor(y + 0.5) and its low word frac(y + 0.5) * 2^32.
+//  * the clamped result (range [LO, HI] around 0x41380000) is
+//    min(max(hi, 0x41380000 + LO), 0x41380000 + HI); its LOW BYTE is the
+//    two's-complement byte of the clamped integer (0x41380000 has a zero low
+//    byte), and every out-of-range t (negative, < 2^20, >= 2^21) clamps to the
+//    correct end;
+//  * near: only for hi inside [0x41380000 + LO, 0x41380000 + HI] (where the
+//    low word is a true fraction), key = frac + m (mod 2^32) is < 2m exactly
+//    when the fraction is within m of 0 or 1; the caller keeps the minimum key.
+template <int LO, int HI>
+__device__ __forceinline__ uint32_t decide_byte(double y, uint32_t mq, uint32_t& kmin) {
   const double t = y + 1572864.5;
-  const int hi = max((int)hi32(t), 0x41300000);
-  const uint32_t fr = lo32(t);
-  dist = min(fr, 0u - fr);
-  return hi - 0x41380000;
+  const int hi = (int)hi32(t);
+  const int c = min(max(hi, 0x41380000 + LO), 0x41380000 + HI);
+  const bool in = (uint32_t)(hi - (0x41380000 + LO)) <= (uint32_t)(HI - LO);
+  const uint32_t key = lo32(t) + mq;
+  kmin = min(kmin, in ? key : 0xFFFFFFFFu);
+  return (uint32_t)c & 0xffu;
 }
 
 // Outputs 4h..4h+3 of the 8-point transform of the integer vector k[0..7]:
@@ -173,7 +182,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 4)
     for (int k = 0; k < 32; ++k) {
       const double a = fabs(m[k]);
       sum += a;
-      nz += ((lo32(m[k]) | (hi32(m[k]) & 0x7FFFFFFFu)) != 0u);
+      nz += (a > 0.0);
       amax = a > amax ? a : amax;
     }
     sh.amax[h][lane] = amax;
@@ -205,22 +214,18 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 4)
     const double A = (1.0 / s) * inv_step;
     const double Bc = -lo * inv_step;
     const uint32_t mq_x = margin32(2.2737367544323206e-13 * (1.0 + fabs(lo) / smax));
-    uint32_t dmin = 0xFFFFFFFFu;  // min distance to a decision boundary that matters
+    if (mq_x >= 0x7FFFFFFFu) status = (status == DERR_NONE) ? NEED_EXACT : status;
+    uint32_t kmin = 0xFFFFFFFFu;  // min over decisions of (frac + m) mod 2^32
 
     // ---- quantizer indices for the 32 own cells ---------------------------
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
       uint32_t word = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t dist;
-        const int n = decide_n(fma(m[w * 4 + q], A, Bc), dist);
-        dmin = min(dmin, (uint32_t)n <= 255u ? dist : 0xFFFFFFFFu);
-        word |= (uint32_t)min(max(n, 0), 255) << (8 * q);
-      }
+      for (int q = 0; q < 4; ++q) word |= decide_byte<0, 255>(fma(m[w * 4 + q], A, Bc), mq_x, kmin) << (8 * q);
       sh.idx[lane][h * 8 + w] = word;
     }
-    bool near = dmin <= mq_x;
+    bool near = kmin < 2u * mq_x;
     pair_bar(bar);    // B3: full index grid visible
 
     // ---- DCT of the index grid: pass 1 (columns, outputs 4h..4h+3) --------
@@ -277,9 +282,10 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 4)
     // ---- retained coefficients (H/codec.hpp:120-123) -----------------------
     const double ps = phi * step;
     const uint32_t mq_c = margin32(phi * 2.0 * Ed + 5.6843418860808015e-14);
+    if (mq_c >= 0x7FFFFFFFu) status = (status == DERR_NONE) ? NEED_EXACT : status;
     const bool zero_c = (status == 0x40u);  // constant block: all coefficients 0
     uint8_t* cb = sh.cbytes + lane * 28;
-    dmin = 0xFFFFFFFFu;
+    kmin = 0xFFFFFFFFu;
     // local rows 0..3, columns 0,1 (both halves): global row r = 4h + ii,
     // k = 8r + c for r < 2, 14 + r (c = 0) / 20 + r (c = 1) otherwise.
 #pragma unroll
@@ -288,25 +294,21 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 4)
       for (int c = 0; c < 2; ++c) {
         const double gv = ii < 2 ? G[ii * 8 + c] : G[16 + (ii - 2) * 2 + c];
         const double y = (h == 0 && ii == 0 && c == 0) ? phi * d00 : gv * ps;
-        uint32_t dist;
-        const int n = decide_n(y, dist);
-        dmin = min(dmin, (uint32_t)(n + 127) <= 254u ? dist : 0xFFFFFFFFu);
+        const uint32_t byte = decide_byte<-127, 127>(y, mq_c, kmin);
         const int r = 4 * h + ii;
         const int k = r < 2 ? 8 * r + c : (c == 0 ? 14 + r : 20 + r);
-        cb[k] = zero_c ? 0 : (uint8_t)min(max(n, -127), 127);
+        cb[k] = zero_c ? 0 : (uint8_t)byte;
       }
     if (h == 0) {  // rows 0,1, columns 2..7
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
         for (int c = 2; c < 8; ++c) {
-          uint32_t dist;
-          const int n = decide_n(G[ii * 8 + c] * ps, dist);
-          dmin = min(dmin, (uint32_t)(n + 127) <= 254u ? dist : 0xFFFFFFFFu);
-          cb[8 * ii + c] = zero_c ? 0 : (uint8_t)min(max(n, -127), 127);
+          const uint32_t byte = decide_byte<-127, 127>(G[ii * 8 + c] * ps, mq_c, kmin);
+          cb[8 * ii + c] = zero_c ? 0 : (uint8_t)byte;
         }
     }
-    near |= dmin <= mq_c;
+    near |= kmin < 2u * mq_c;
     if (h == 1) sh.nearL[lane] = near ? 1u : 0u;
     pair_bar(bar);    // B5: coefficient bytes and the lower near flag visible
 
