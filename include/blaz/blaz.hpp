@@ -29,7 +29,10 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <istream>
+#include <iterator>
 #include <mutex>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -99,6 +102,12 @@ struct compressed_matrix {
     const compressed_block& block(std::size_t br, std::size_t bc) const { return blocks[br * block_cols + bc]; }
 };
 
+// File-format failures (H/io.hpp:20-23).
+class io_error : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
 struct partial_reconstruction {
     block8 values;
     int extent = 0;
@@ -124,6 +133,7 @@ inline void check(blz_status st) {
     if (st == BLZ_INVALID_ARGUMENT) throw std::invalid_argument(msg);
     if (st == BLZ_OUT_OF_RANGE) throw std::out_of_range(msg);
     if (st == BLZ_OUT_OF_MEMORY) throw std::bad_alloc();
+    if (st == BLZ_IO_ERROR) throw io_error(msg);
     throw std::runtime_error("blaz: " + msg);
 }
 
@@ -278,6 +288,27 @@ inline block8 block_mul(const compressed_block& b1, const compressed_block& b2) 
     block8 out;
     gpu::check(blz_mat_mul_dense(gpu::context(), gpu::raw(&b1), 8, 8, gpu::raw(&b2), 8, 8, out.a.data(), 1));
     return out;
+}
+
+// ---- .blzc container (H/io.hpp:93-134), packed/validated on the GPU ----------------
+inline std::size_t write_compressed(const compressed_matrix& cm, std::ostream& out) {
+    std::vector<std::uint8_t> bytes(blz_blzc_bytes(cm.rows, cm.cols));
+    std::uint64_t n = 0;
+    gpu::check(blz_write_compressed(gpu::context(), gpu::raw(cm.blocks.data()), cm.rows, cm.cols, bytes.data(),
+                                    bytes.size(), &n));
+    out.write(reinterpret_cast<const char*>(bytes.data()), std::streamsize(n));
+    if (!out) throw io_error("write_compressed: write failed");
+    return std::size_t(n);
+}
+
+inline compressed_matrix read_compressed(std::istream& in) {
+    const std::vector<std::uint8_t> bytes{std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>()};
+    std::uint64_t rows = 0, cols = 0;
+    gpu::check(blz_read_compressed(gpu::context(), bytes.data(), bytes.size(), &rows, &cols, nullptr, 0));
+    compressed_matrix cm = gpu::shaped(rows, cols);
+    gpu::check(blz_read_compressed(gpu::context(), bytes.data(), bytes.size(), &rows, &cols,
+                                   gpu::raw(cm.blocks.data()), cm.blocks.size()));
+    return cm;
 }
 
 // ---- uncompressed baselines (H/matrix.hpp:253-300), CPU ---------------------------

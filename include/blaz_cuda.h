@@ -43,7 +43,8 @@ typedef enum blz_status {
     BLZ_OUT_OF_RANGE = 2,     /* std::out_of_range in the reference */
     BLZ_CUDA_ERROR = 3,
     BLZ_OUT_OF_MEMORY = 4,
-    BLZ_NOT_SUPPORTED = 5
+    BLZ_NOT_SUPPORTED = 5,
+    BLZ_IO_ERROR = 6          /* blaz::io_error in the reference (H/io.hpp:20-23) */
 } blz_status;
 
 /* Reference compressed_block (H/block.hpp:33-38), 48 bytes in memory:
@@ -187,6 +188,24 @@ blz_status blz_compress_blocks(blz_ctx* ctx, const double* tiles, uint64_t n, bl
 blz_status blz_decompress_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, double* tiles);
 /* dequantize_prediction (H/codec.hpp:150-158): the 8x8 slope grid of each block. */
 blz_status blz_dequantize_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, double* tiles);
+
+/* ---- .blzc container (H/io.hpp:93-134) --------------------------------------- */
+/* 13-byte header ("BLZC", version 1, rows, cols as LE u32) + 45-byte records
+ * (f, s LE binary64, scale byte, 28 coefficients) in row-major block order. */
+uint64_t blz_blzc_bytes(uint64_t rows, uint64_t cols);
+/* write_compressed on the device: `out` (device) receives blz_blzc_bytes bytes;
+ * a non-finite f or s latches "write_compressed: non-finite block field". */
+blz_status blz_pack_blzc_dev(blz_ctx* ctx, const blz_cmat* in, uint8_t* out);
+/* read_compressed on the device (synchronizes for the header): validates
+ * magic, version, zero dims, zero scale factors and truncation with the
+ * reference's messages; `out` must have the header's dimensions. */
+blz_status blz_unpack_blzc_dev(blz_ctx* ctx, const uint8_t* in, uint64_t nbytes, const blz_cmat* out);
+/* Host-buffer variants.  blz_read_compressed with out == NULL only parses the
+ * header into rows/cols. */
+blz_status blz_write_compressed(blz_ctx* ctx, const blz_block* blocks, uint64_t rows, uint64_t cols,
+                                uint8_t* out, uint64_t capacity, uint64_t* written);
+blz_status blz_read_compressed(blz_ctx* ctx, const uint8_t* bytes, uint64_t nbytes, uint64_t* rows,
+                               uint64_t* cols, blz_block* out, uint64_t out_capacity);
 
 #ifdef __cplusplus
 }

@@ -266,6 +266,8 @@ class Ref:
         self._mdot = L.fn("mat_dot", C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _P])
         self._mm = L.fn("mat_mul", C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, C.c_uint, _P])
         self._mmd = L.fn("mat_mul_dense", C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, C.c_uint, _P])
+        self._wc = L.fn("write_compressed", C.c_longlong, [_P, _SZ, _SZ, _P, _SZ])
+        self._rc = L.fn("read_compressed", C.c_int, [_P, _SZ, C.POINTER(_SZ), C.POINTER(_SZ), _P, _SZ])
         # handle API (timing)
         self.dense_new = L.fn("dense_new", _P, [_P, _SZ, _SZ])
         self.dense_free = L.fn("dense_free", None, [_P])
@@ -378,6 +380,24 @@ class Ref:
         out = np.zeros((ar, bc), np.float64)
         self._check(self._mmd(_ptr(a), ar, ac, _ptr(b), br, bc, threads, _ptr(out)))
         return out
+
+    def write_compressed(self, blocks, rows, cols) -> bytes:
+        blocks = np.ascontiguousarray(blocks, BLOCK_DTYPE)
+        cap = 13 + 45 * blocks.size
+        buf = np.zeros(cap, np.uint8)
+        n = self._wc(_ptr(blocks), rows, cols, _ptr(buf), cap)
+        if n < 0:
+            raise OracleError(3, self._err().decode())
+        return buf[:n].tobytes()
+
+    def read_compressed(self, data: bytes):
+        raw = np.frombuffer(data, np.uint8).copy()
+        rows, cols = _SZ(), _SZ()
+        cap = max(1, (len(data) // 45) + 1)
+        out = np.zeros(cap, BLOCK_DTYPE)
+        self._check(self._rc(_ptr(raw), raw.size, C.byref(rows), C.byref(cols), _ptr(out), cap))
+        nb = _nb(rows.value) * _nb(cols.value)
+        return rows.value, cols.value, out[:nb].copy()
 
 
 def port() -> Port:

@@ -12,6 +12,7 @@
 // blaz::compressed_block (H/block.hpp:33-38).
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -165,6 +166,31 @@ int ref_mat_mul_dense(const blaz::compressed_block* a, std::size_t ar, std::size
     return run([&] {
         const auto r = blaz::mat_mul_dense(make_cm(a, ar, ac), make_cm(b, br, bc), threads);
         std::memcpy(out, r.values.data(), r.values.size() * sizeof(double));
+    });
+}
+
+// ---- .blzc container through the reference's io.hpp (H/io.hpp:93-134) ------
+long long ref_write_compressed(const blaz::compressed_block* blocks, std::size_t rows, std::size_t cols,
+                               unsigned char* out, std::size_t cap) {
+    long long n = -1;
+    const int st = run([&] {
+        std::ostringstream os;
+        blaz::write_compressed(make_cm(blocks, rows, cols), os);
+        const std::string b = os.str();
+        if (b.size() <= cap) std::memcpy(out, b.data(), b.size());
+        n = (long long)b.size();
+    });
+    return st ? -1 : n;
+}
+
+int ref_read_compressed(const unsigned char* bytes, std::size_t n, std::size_t* rows, std::size_t* cols,
+                        blaz::compressed_block* out, std::size_t cap) {
+    return run([&] {
+        std::istringstream is(std::string(reinterpret_cast<const char*>(bytes), n));
+        const auto cm = blaz::read_compressed(is);
+        *rows = cm.rows;
+        *cols = cm.cols;
+        if (cm.blocks.size() <= cap) std::memcpy(out, cm.blocks.data(), cm.blocks.size() * sizeof(blaz::compressed_block));
     });
 }
 

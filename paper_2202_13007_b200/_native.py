@@ -20,7 +20,7 @@ BLOCK_DTYPE = np.dtype(
      "formats": ["<f8", "<f8", "u1", ("i1", 28)],
      "offsets": [0, 8, 16, 17], "itemsize": 48})
 
-BLZ_OK, BLZ_INVALID_ARGUMENT, BLZ_OUT_OF_RANGE, BLZ_CUDA_ERROR, BLZ_OUT_OF_MEMORY, BLZ_NOT_SUPPORTED = range(6)
+BLZ_OK, BLZ_INVALID_ARGUMENT, BLZ_OUT_OF_RANGE, BLZ_CUDA_ERROR, BLZ_OUT_OF_MEMORY, BLZ_NOT_SUPPORTED, BLZ_IO_ERROR = range(7)
 GEMM_EXACT, GEMM_FUSED = 0, 1
 MODE_DEFAULT, MODE_EXACT = 0, 1
 
@@ -35,6 +35,10 @@ class InvalidArgument(ValueError):
 
 class OutOfRange(IndexError):
     """std::out_of_range in the reference."""
+
+
+class IoError(RuntimeError):
+    """blaz::io_error (H/io.hpp:20-23)."""
 
 
 class NotBuilt(ImportError):
@@ -97,6 +101,11 @@ SIGNATURES = {
     "blz_compress_blocks": (_ST, [_P, _P, _U64, _P]),
     "blz_decompress_blocks": (_ST, [_P, _P, _U64, _P]),
     "blz_dequantize_blocks": (_ST, [_P, _P, _U64, _P]),
+    "blz_blzc_bytes": (_U64, [_U64, _U64]),
+    "blz_pack_blzc_dev": (_ST, [_P, C.POINTER(blz_cmat), _P]),
+    "blz_unpack_blzc_dev": (_ST, [_P, _P, _U64, C.POINTER(blz_cmat)]),
+    "blz_write_compressed": (_ST, [_P, _P, _U64, _U64, _P, _U64, C.POINTER(_U64)]),
+    "blz_read_compressed": (_ST, [_P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64), _P, _U64]),
 }
 
 _lib = None
@@ -130,6 +139,8 @@ def raise_for(status: int, ctx_handle) -> None:
         raise InvalidArgument(msg)
     if status == BLZ_OUT_OF_RANGE:
         raise OutOfRange(msg)
+    if status == BLZ_IO_ERROR:
+        raise IoError(msg)
     if status == BLZ_OUT_OF_MEMORY:
         raise MemoryError(msg)
     raise BlazError(f"status {status}: {msg}")

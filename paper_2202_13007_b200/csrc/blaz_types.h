@@ -28,4 +28,6 @@ namespace blz {
 constexpr unsigned DERR_NONFINITE_CODE = 1;  // "normalize: non-finite input"          H/codec.hpp:21
 constexpr unsigned DERR_PREDICT_CODE = 2;    // "predict: mean slope must be positive" H/codec.hpp:86
 constexpr unsigned DERR_DOT_RANGE_CODE = 3;  // "mat_dot: index out of range"          H/matrix.hpp:160
+constexpr unsigned DERR_IO_NONFINITE_CODE = 4;  // "write_compressed: non-finite block field" H/io.hpp:102-103
+constexpr unsigned DERR_IO_ZERO_PHI_CODE = 5;   // "compressed matrix: zero scale factor in block t" H/io.hpp:129-130
 }  // namespace blz

@@ -192,6 +192,10 @@ blz_status latch_status(blz_ctx* c) {
       return set_err(c, BLZ_INVALID_ARGUMENT, "predict: mean slope must be positive");
     case blz::DERR_DOT_RANGE_CODE:
       return set_err(c, BLZ_OUT_OF_RANGE, "mat_dot: index out of range");
+    case blz::DERR_IO_NONFINITE_CODE:
+      return set_err(c, BLZ_IO_ERROR, "write_compressed: non-finite block field");
+    case blz::DERR_IO_ZERO_PHI_CODE:
+      return set_err(c, BLZ_IO_ERROR, "compressed matrix: zero scale factor in block " + std::to_string(v >> 8));
     default:
       return set_err(c, BLZ_CUDA_ERROR, "unknown device error");
   }
@@ -688,6 +692,95 @@ blz_status blz_dequantize_blocks(blz_ctx* c, const blz_block* in, uint64_t n, do
   if (!d) return cuda_err(c, e, "scratch allocation");
   BLZ_CUDA(c, blz::launch_dequantize(lc(c), c->basis, view(&m), d), "dequantize");
   BLZ_CUDA(c, cudaMemcpyAsync(tiles, d, n * 64 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  return latch_status(c);
+}
+
+// ---- .blzc container (H/io.hpp:93-134) ---------------------------------------------
+uint64_t blz_blzc_bytes(uint64_t rows, uint64_t cols) { return 13 + 45 * nblk(rows) * nblk(cols); }
+
+blz_status blz_pack_blzc_dev(blz_ctx* c, const blz_cmat* in, uint8_t* out) {
+  if (!c || !out) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, in, "write_compressed")) return st;
+  return cuda_err(c, blz::launch_pack_blzc(lc(c), view(in), out), "write_compressed");
+}
+
+// Header checks of read_header (H/io.hpp:78-89) on the 13 host bytes.
+static blz_status parse_header(blz_ctx* c, const uint8_t* h, uint64_t nbytes, uint64_t* rows, uint64_t* cols) {
+  const std::string kind = "compressed matrix";
+  if (nbytes < 13) return set_err(c, BLZ_IO_ERROR, kind + ": truncated header");
+  if (std::memcmp(h, "BLZC", 4) != 0)
+    return set_err(c, BLZ_IO_ERROR, kind + ": magic mismatch (not a " + kind + " file)");
+  if (h[4] != 1) return set_err(c, BLZ_IO_ERROR, kind + ": unsupported version " + std::to_string(h[4]));
+  auto u32 = [](const uint8_t* p) {
+    return (uint64_t)p[0] | (uint64_t)p[1] << 8 | (uint64_t)p[2] << 16 | (uint64_t)p[3] << 24;
+  };
+  *rows = u32(h + 5);
+  *cols = u32(h + 9);
+  if (*rows == 0 || *cols == 0) return set_err(c, BLZ_IO_ERROR, kind + ": zero dimension in header");
+  return BLZ_OK;
+}
+
+// Unpacks a device byte stream into `out` (dims must match the header).  A
+// zero scale factor in an earlier block is reported before a truncation, as
+// the reference's sequential reader does (H/io.hpp:121-132).
+static blz_status unpack_stream(blz_ctx* c, const uint8_t* dev_bytes, uint64_t nbytes, const blz_cmat* out) {
+  const uint64_t nb = out->block_rows * out->block_cols;
+  const uint64_t avail = (nbytes - 13) / 45;
+  BLZ_CUDA(c, blz::launch_unpack_blzc(lc(c), dev_bytes, view(out), avail), "read_compressed");
+  if (blz_status st = latch_status(c)) return st;
+  if (avail < nb)
+    return set_err(c, BLZ_IO_ERROR, "compressed matrix: truncated at block " + std::to_string(avail));
+  return BLZ_OK;
+}
+
+blz_status blz_unpack_blzc_dev(blz_ctx* c, const uint8_t* in, uint64_t nbytes, const blz_cmat* out) {
+  if (!c || !in) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, out, "read_compressed")) return st;
+  uint8_t h[13] = {0};
+  if (nbytes >= 13)
+    BLZ_CUDA(c, cudaMemcpyAsync(h, in, 13, cudaMemcpyDeviceToHost, c->stream), "read_compressed header");
+  BLZ_CUDA(c, cudaStreamSynchronize(c->stream), "sync");
+  uint64_t rows = 0, cols = 0;
+  if (blz_status st = parse_header(c, h, nbytes, &rows, &cols)) return st;
+  if (rows != out->rows || cols != out->cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "read_compressed: output dimension mismatch");
+  return unpack_stream(c, in, nbytes, out);
+}
+
+blz_status blz_write_compressed(blz_ctx* c, const blz_block* blocks, uint64_t rows, uint64_t cols, uint8_t* out,
+                                uint64_t capacity, uint64_t* written) {
+  if (!c || !out) return BLZ_INVALID_ARGUMENT;
+  const uint64_t need = blz_blzc_bytes(rows, cols);
+  if (capacity < need) return set_err(c, BLZ_INVALID_ARGUMENT, "write_compressed: output buffer too small");
+  blz_cmat m;
+  if (blz_status st = upload_blocks(c, blocks, rows, cols, S_CM0, &m)) return st;
+  cudaError_t e;
+  uint8_t* d = (uint8_t*)slot(c, S_OUT, need, &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  if (blz_status st = blz_pack_blzc_dev(c, &m, d)) return st;
+  if (blz_status st = latch_status(c)) return st;
+  BLZ_CUDA(c, cudaMemcpyAsync(out, d, need, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  BLZ_CUDA(c, cudaStreamSynchronize(c->stream), "sync");
+  if (written) *written = need;
+  return BLZ_OK;
+}
+
+blz_status blz_read_compressed(blz_ctx* c, const uint8_t* bytes, uint64_t nbytes, uint64_t* rows, uint64_t* cols,
+                               blz_block* out, uint64_t out_capacity) {
+  if (!c || !bytes || !rows || !cols) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = parse_header(c, bytes, nbytes, rows, cols)) return st;
+  if (!out) return BLZ_OK;  // dimension query
+  const uint64_t nb = nblk(*rows) * nblk(*cols);
+  if (out_capacity < nb) return set_err(c, BLZ_INVALID_ARGUMENT, "read_compressed: output buffer too small");
+  cudaError_t e;
+  const uint64_t take = nbytes < blz_blzc_bytes(*rows, *cols) ? nbytes : blz_blzc_bytes(*rows, *cols);
+  uint8_t* d = (uint8_t*)slot(c, S_IN0, take, &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  BLZ_CUDA(c, cudaMemcpyAsync(d, bytes, take, cudaMemcpyHostToDevice, c->stream), "H2D");
+  blz_cmat m;
+  if (blz_status st = scratch_cmat(c, S_CM0, *rows, *cols, &m)) return st;
+  if (blz_status st = unpack_stream(c, d, take, &m)) return st;
+  if (blz_status st = download_blocks(c, &m, out)) return st;
   return latch_status(c);
 }
 

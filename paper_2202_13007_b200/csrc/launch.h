@@ -47,6 +47,9 @@ cudaError_t launch_unpack_aos(const LaunchCtx& c, const void* aos, const CMat& o
 // addsub.cu (coalesced warp-staged variants; false if the SoA arrays are not 16-byte aligned)
 bool launch_addsub_v2(const LaunchCtx& c, bool sub, const CMat& a, const CMat& b, const CMat& out, cudaError_t* err);
 bool launch_scale_v2(const LaunchCtx& c, const CMat& a, double k, const CMat& out, cudaError_t* err);
+// io.cu (.blzc container)
+cudaError_t launch_pack_blzc(const LaunchCtx& c, const CMat& in, uint8_t* out);
+cudaError_t launch_unpack_blzc(const LaunchCtx& c, const uint8_t* in, const CMat& out, uint64_t nlimit);
 // dot.cu
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out);

@@ -33,7 +33,7 @@ import threading
 import numpy as np
 
 from . import _native as N
-from ._native import BLOCK_DTYPE, InvalidArgument, OutOfRange  # noqa: F401
+from ._native import BLOCK_DTYPE, InvalidArgument, IoError, OutOfRange  # noqa: F401
 
 block_dim = 8
 block_cells = 64
@@ -253,3 +253,27 @@ def compress_block(tile, ctx: Context | None = None):
 
 def decompress_block(block, ctx: Context | None = None) -> np.ndarray:
     return decompress_blocks(np.array([block], BLOCK_DTYPE), ctx)[0]
+
+
+def write_compressed(cm: CompressedMatrix, ctx: Context | None = None) -> bytes:
+    """write_compressed (H/io.hpp:96-111): the .blzc byte stream, packed on the GPU."""
+    ctx = ctx or default_context()
+    b = _blocks(cm)
+    n = int(ctx.lib.blz_blzc_bytes(cm.rows, cm.cols))
+    out = np.zeros(n, np.uint8)
+    written = C.c_uint64()
+    ctx.check(ctx.lib.blz_write_compressed(ctx.handle, _ptr(b), cm.rows, cm.cols, _ptr(out), n, C.byref(written)))
+    return out[: written.value].tobytes()
+
+
+def read_compressed(data: bytes, ctx: Context | None = None) -> CompressedMatrix:
+    """read_compressed (H/io.hpp:113-134): parses and validates on the GPU;
+    malformed input raises IoError with the reference's message."""
+    ctx = ctx or default_context()
+    raw = np.frombuffer(bytes(data), np.uint8).copy()
+    rows, cols = C.c_uint64(), C.c_uint64()
+    ctx.check(ctx.lib.blz_read_compressed(ctx.handle, _ptr(raw), raw.size, C.byref(rows), C.byref(cols), None, 0))
+    out = np.zeros((_nb(rows.value), _nb(cols.value)), BLOCK_DTYPE)
+    ctx.check(ctx.lib.blz_read_compressed(ctx.handle, _ptr(raw), raw.size, C.byref(rows), C.byref(cols), _ptr(out),
+                                          out.size))
+    return CompressedMatrix(rows.value, cols.value, out)

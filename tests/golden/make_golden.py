@@ -128,6 +128,8 @@ def main():
         for v in rd:
             tot = tot + float(v)
         g[f"m{n}_rowdot"], g[f"m{n}_frob"] = rd, np.array(tot)
+        # .blzc container bytes written by the reference (H/io.hpp:96-111)
+        g[f"m{n}_blzc"] = np.frombuffer(r.write_compressed(ca, rows, cols), np.uint8)
     g["shapes"] = np.array(shapes)
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")

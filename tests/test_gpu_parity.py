@@ -287,3 +287,52 @@ def test_matmul_fused_dmma_tolerance(port):
     err = np.max(np.abs(fused - exact)) / max(1.0, np.max(np.abs(exact)))
     assert err <= 1e-13 * 512, err
     assert np.array_equal(bits(fused), bits(dev.matmul_dense(A, B, mode=blz.GEMM_FUSED).cpu().numpy()))  # deterministic
+
+
+# ---- .blzc container (H/io.hpp:93-134) --------------------------
+@pytest.mark.parametrize("n", range(10))
+def test_blzc_bytes_match_reference(golden, n):
+    rows, cols = (int(v) for v in golden["shapes"][n])
+    cm = blz.CompressedMatrix(rows, cols, golden[f"m{n}_ca"])
+    data = blz.write_compressed(cm)
+    assert data == golden[f"m{n}_blzc"].tobytes()            # byte-identical to the reference writer
+    back = blz.read_compressed(data)
+    assert (back.rows, back.cols) == (rows, cols)
+    assert blocks_equal(back.blocks, cm.blocks)
+
+
+def test_blzc_device_roundtrip_large():
+    a = W.quadratic_blocks(2048, 2056, seed=51)
+    A = dev.compress(a.cuda())
+    ctx = dev.context()
+    n = int(ctx.lib.blz_blzc_bytes(A.rows, A.cols))
+    buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+    import ctypes as C
+    ctx.check(ctx.lib.blz_pack_blzc_dev(ctx.handle, A.ref(), C.c_void_p(buf.data_ptr())))
+    B = dev.DeviceCMat(A.rows, A.cols)
+    ctx.check(ctx.lib.blz_unpack_blzc_dev(ctx.handle, C.c_void_p(buf.data_ptr()), n, B.ref()))
+    assert blocks_equal(B.to_host().blocks, A.to_host().blocks)
+    assert buf.cpu().numpy().tobytes() == blz.write_compressed(A.to_host())
+
+
+def test_blzc_errors_match_reference(golden):
+    good = golden["m7_blzc"].tobytes()  # 40 x 56 -> 35 blocks
+    cases = [
+        (good[:5], "compressed matrix: truncated header"),
+        (b"XLZC" + good[4:], r"compressed matrix: magic mismatch \(not a compressed matrix file\)"),
+        (good[:4] + bytes([2]) + good[5:], "compressed matrix: unsupported version 2"),
+        (good[:5] + bytes(4) + good[9:], "compressed matrix: zero dimension in header"),
+        (good[:13 + 45 * 10 + 7], "compressed matrix: truncated at block 10"),
+    ]
+    zero_phi = bytearray(good)
+    zero_phi[13 + 45 * 3 + 16] = 0
+    cases.append((bytes(zero_phi), "compressed matrix: zero scale factor in block 3"))
+    both = bytearray(zero_phi[:13 + 45 * 20])  # zero phi at block 3 reported before truncation at 20
+    cases.append((bytes(both), "compressed matrix: zero scale factor in block 3"))
+    for data, msg in cases:
+        with pytest.raises(blz.IoError, match=msg):
+            blz.read_compressed(data)
+    bad = blz.CompressedMatrix(8, 8, golden["m1_ca"].copy())
+    bad.blocks["slope"][0, 0] = np.inf
+    with pytest.raises(blz.IoError, match="write_compressed: non-finite block field"):
+        blz.write_compressed(bad)
