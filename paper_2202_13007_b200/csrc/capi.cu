@@ -6,6 +6,7 @@
 // kernel launched here.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -31,6 +32,9 @@ struct blz_ctx {
   unsigned long long* d_stats = nullptr;  // [0] compress exact-path blocks, [1] add/sub dense fallbacks
   uint64_t* d_wl = nullptr;               // exact-path worklist: 256 B counter + capacity entries
   uint64_t wl_cap = 0;
+  // host-level pipelining: copy-in / copy-out streams and per-chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> events;
   // grow-only device scratch slots (host-level calls, add fallback worklist)
   struct Slot {
     void* p = nullptr;
@@ -271,6 +275,9 @@ void blz_ctx_destroy(blz_ctx* c) {
   if (c->d_err) cudaFree(c->d_err);
   if (c->d_stats) cudaFree(c->d_stats);
   if (c->d_wl) cudaFree(c->d_wl);
+  if (c->s_in) cudaStreamDestroy(c->s_in);
+  if (c->s_out) cudaStreamDestroy(c->s_out);
+  for (auto ev : c->events) cudaEventDestroy(ev);
   delete c;
 }
 
@@ -509,6 +516,73 @@ blz_status blz_unpack_aos_dev(blz_ctx* c, const blz_block* in, const blz_cmat* o
 }
 
 // ---- host-level drop-in entry points ------------------------------------------
+// The big host-level calls are pipelined over block-row chunks: the upload of
+// chunk i+1 (copy-in stream), the kernels of chunk i (context stream) and the
+// download of chunk i-1 (copy-out stream) overlap, so a call costs about its
+// larger PCIe direction instead of the sum of both plus the kernels.  Chunks
+// start at multiples of 16 block-rows, which keeps every SoA sub-view 16-byte
+// aligned for the vectorized kernels.
+
+}  // extern "C"
+
+namespace {
+
+blz_cmat sub_rows(const blz_cmat& m, uint64_t b0, uint64_t b1) {
+  blz_cmat v = m;
+  const uint64_t off = b0 * m.block_cols;
+  v.rows = std::min(m.rows, 8 * b1) - 8 * b0;
+  v.block_rows = b1 - b0;
+  v.first = m.first + off;
+  v.slope = m.slope + off;
+  v.coeffs = m.coeffs + 28 * off;
+  v.scale = m.scale + off;
+  return v;
+}
+
+blz_status ensure_pipe(blz_ctx* c, size_t nev) {
+  if (!c->s_in) BLZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking), "stream");
+  if (!c->s_out) BLZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking), "stream");
+  while (c->events.size() < nev) {
+    cudaEvent_t ev;
+    BLZ_CUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    c->events.push_back(ev);
+  }
+  return BLZ_OK;
+}
+
+template <class H2D, class Compute, class D2H>
+blz_status pipelined(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compute, D2H&& d2h) {
+  uint64_t step = (block_rows + 15) / 16;
+  step = (step + 15) / 16 * 16;
+  if (step < 16) step = 16;
+  const uint64_t nchunks = (block_rows + step - 1) / step;
+  if (blz_status st = ensure_pipe(c, 2 * nchunks + 1)) return st;
+  // uploads must not overtake earlier work queued on the context stream
+  BLZ_CUDA(c, cudaEventRecord(c->events[2 * nchunks], c->stream), "event");
+  BLZ_CUDA(c, cudaStreamWaitEvent(c->s_in, c->events[2 * nchunks], 0), "event");
+  for (uint64_t i = 0; i < nchunks; ++i) {
+    const uint64_t b0 = i * step, b1 = std::min(block_rows, b0 + step);
+    cudaEvent_t in_done = c->events[2 * i], k_done = c->events[2 * i + 1];
+    BLZ_CUDA(c, h2d(b0, b1, c->s_in), "H2D");
+    BLZ_CUDA(c, cudaEventRecord(in_done, c->s_in), "event");
+    BLZ_CUDA(c, cudaStreamWaitEvent(c->stream, in_done, 0), "event");
+    if (blz_status st = compute(b0, b1)) return st;
+    BLZ_CUDA(c, cudaEventRecord(k_done, c->stream), "event");
+    BLZ_CUDA(c, cudaStreamWaitEvent(c->s_out, k_done, 0), "event");
+    BLZ_CUDA(c, d2h(b0, b1, c->s_out), "D2H");
+  }
+  BLZ_CUDA(c, cudaStreamSynchronize(c->s_out), "sync");
+  BLZ_CUDA(c, cudaStreamSynchronize(c->s_in), "sync");
+  return BLZ_OK;
+}
+
+// device AoS staging for block-row range [b0, b1) of a (rows x cols) grid
+blz_block* aos_at(void* base, uint64_t b0, uint64_t bc) { return (blz_block*)base + b0 * bc; }
+
+}  // namespace
+
+extern "C" {
+
 blz_status blz_compress_matrix(blz_ctx* c, const double* values, uint64_t rows, uint64_t cols, blz_block* out,
                                unsigned threads) {
   (void)threads;
@@ -517,11 +591,29 @@ blz_status blz_compress_matrix(blz_ctx* c, const double* values, uint64_t rows, 
   cudaError_t e;
   double* d = (double*)slot(c, S_IN0, rows * cols * sizeof(double), &e);
   if (!d) return cuda_err(c, e, "scratch allocation");
-  BLZ_CUDA(c, cudaMemcpyAsync(d, values, rows * cols * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
   blz_cmat m;
   if (blz_status st = scratch_cmat(c, S_CM0, rows, cols, &m)) return st;
-  if (blz_status st = blz_compress_dev(c, d, rows, cols, cols, &m)) return st;
-  if (blz_status st = download_blocks(c, &m, out)) return st;
+  const uint64_t bc = m.block_cols;
+  void* aos = slot(c, S_AUX, m.block_rows * bc * sizeof(blz_block), &e);
+  if (!aos) return cuda_err(c, e, "scratch allocation");
+  if (blz_status st = ensure_worklist(c, m.block_rows * bc)) return st;
+  auto rows_of = [&](uint64_t b0, uint64_t b1) { return std::min(rows, 8 * b1) - 8 * b0; };
+  blz_status st = pipelined(
+      c, m.block_rows,
+      [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        return cudaMemcpyAsync(d + 8 * b0 * cols, values + 8 * b0 * cols, rows_of(b0, b1) * cols * sizeof(double),
+                               cudaMemcpyHostToDevice, s);
+      },
+      [&](uint64_t b0, uint64_t b1) {
+        const blz_cmat v = sub_rows(m, b0, b1);
+        if (blz_status st2 = blz_compress_dev(c, d + 8 * b0 * cols, v.rows, cols, cols, &v)) return st2;
+        return blz_pack_aos_dev(c, &v, aos_at(aos, b0, bc));
+      },
+      [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        return cudaMemcpyAsync(out + b0 * bc, aos_at(aos, b0, bc), (b1 - b0) * bc * sizeof(blz_block),
+                               cudaMemcpyDeviceToHost, s);
+      });
+  if (st) return st;
   return latch_status(c);
 }
 
@@ -531,13 +623,73 @@ blz_status blz_decompress_matrix(blz_ctx* c, const blz_block* in, uint64_t rows,
   if (!c) return BLZ_INVALID_ARGUMENT;
   if (rows == 0 || cols == 0) return BLZ_OK;
   blz_cmat m;
-  if (blz_status st = upload_blocks(c, in, rows, cols, S_CM0, &m)) return st;
+  if (blz_status st = scratch_cmat(c, S_CM0, rows, cols, &m)) return st;
+  const uint64_t bc = m.block_cols;
   cudaError_t e;
+  void* aos = slot(c, S_AUX, m.block_rows * bc * sizeof(blz_block), &e);
+  if (!aos) return cuda_err(c, e, "scratch allocation");
   double* d = (double*)slot(c, S_OUT, rows * cols * sizeof(double), &e);
   if (!d) return cuda_err(c, e, "scratch allocation");
-  if (blz_status st = blz_decompress_dev(c, &m, d, cols)) return st;
-  BLZ_CUDA(c, cudaMemcpyAsync(out, d, rows * cols * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  auto rows_of = [&](uint64_t b0, uint64_t b1) { return std::min(rows, 8 * b1) - 8 * b0; };
+  blz_status st = pipelined(
+      c, m.block_rows,
+      [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        return cudaMemcpyAsync(aos_at(aos, b0, bc), in + b0 * bc, (b1 - b0) * bc * sizeof(blz_block),
+                               cudaMemcpyHostToDevice, s);
+      },
+      [&](uint64_t b0, uint64_t b1) {
+        const blz_cmat v = sub_rows(m, b0, b1);
+        if (blz_status st2 = blz_unpack_aos_dev(c, aos_at(aos, b0, bc), &v)) return st2;
+        return blz_decompress_dev(c, &v, d + 8 * b0 * cols, cols);
+      },
+      [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        return cudaMemcpyAsync(out + 8 * b0 * cols, d + 8 * b0 * cols, rows_of(b0, b1) * cols * sizeof(double),
+                               cudaMemcpyDeviceToHost, s);
+      });
+  if (st) return st;
   return latch_status(c);
+}
+
+// Shared body of mat_add / mat_sub / mat_scale on host records (k unused for add/sub).
+static blz_status elementwise_host(blz_ctx* c, int op, const blz_block* a, const blz_block* b, uint64_t rows,
+                                   uint64_t cols, double k, blz_block* out) {
+  blz_cmat ma, mb, mo;
+  if (blz_status st = scratch_cmat(c, S_CM0, rows, cols, &ma)) return st;
+  if (op != 2)
+    if (blz_status st = scratch_cmat(c, S_CM1, rows, cols, &mb)) return st;
+  if (blz_status st = scratch_cmat(c, S_CM2, rows, cols, &mo)) return st;
+  const uint64_t bc = ma.block_cols, nb = ma.block_rows * bc;
+  cudaError_t e;
+  // AoS staging: inputs a | b, output o (3 regions)
+  blz_block* aos = (blz_block*)slot(c, S_AUX, 3 * nb * sizeof(blz_block), &e);
+  if (!aos) return cuda_err(c, e, "scratch allocation");
+  blz_block *sa = aos, *sb = aos + nb, *so = aos + 2 * nb;
+  if (op != 2)
+    if (blz_status st = ensure_worklist(c, nb)) return st;
+  return pipelined(
+      c, ma.block_rows,
+      [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        const size_t n = (b1 - b0) * bc * sizeof(blz_block);
+        cudaError_t e2 = cudaMemcpyAsync(sa + b0 * bc, a + b0 * bc, n, cudaMemcpyHostToDevice, s);
+        if (e2 == cudaSuccess && op != 2) e2 = cudaMemcpyAsync(sb + b0 * bc, b + b0 * bc, n, cudaMemcpyHostToDevice, s);
+        return e2;
+      },
+      [&](uint64_t b0, uint64_t b1) {
+        const blz_cmat va = sub_rows(ma, b0, b1), vo = sub_rows(mo, b0, b1);
+        if (blz_status st2 = blz_unpack_aos_dev(c, sa + b0 * bc, &va)) return st2;
+        if (op == 2) {
+          if (blz_status st2 = blz_scale_dev(c, &va, k, &vo)) return st2;
+        } else {
+          const blz_cmat vb = sub_rows(mb, b0, b1);
+          if (blz_status st2 = blz_unpack_aos_dev(c, sb + b0 * bc, &vb)) return st2;
+          if (blz_status st2 = addsub_dev(c, op == 1, &va, &vb, &vo)) return st2;
+        }
+        return blz_pack_aos_dev(c, &vo, so + b0 * bc);
+      },
+      [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        return cudaMemcpyAsync(out + b0 * bc, so + b0 * bc, (b1 - b0) * bc * sizeof(blz_block),
+                               cudaMemcpyDeviceToHost, s);
+      });
 }
 
 static blz_status mat_addsub_host(blz_ctx* c, bool sub, const blz_block* a, uint64_t ar, uint64_t ac,
@@ -545,12 +697,7 @@ static blz_status mat_addsub_host(blz_ctx* c, bool sub, const blz_block* a, uint
   if (!c) return BLZ_INVALID_ARGUMENT;
   if (blz_status st = same_dims(c, ar, ac, br, bc, sub ? "mat_sub" : "mat_add")) return st;
   if (ar == 0 || ac == 0) return BLZ_OK;
-  blz_cmat ma, mb, mo;
-  if (blz_status st = upload_blocks(c, a, ar, ac, S_CM0, &ma)) return st;
-  if (blz_status st = upload_blocks(c, b, br, bc, S_CM1, &mb)) return st;
-  if (blz_status st = scratch_cmat(c, S_CM2, ar, ac, &mo)) return st;
-  if (blz_status st = addsub_dev(c, sub, &ma, &mb, &mo)) return st;
-  if (blz_status st = download_blocks(c, &mo, out)) return st;
+  if (blz_status st = elementwise_host(c, sub ? 1 : 0, a, b, ar, ac, 0.0, out)) return st;
   return latch_status(c);
 }
 
@@ -572,11 +719,7 @@ blz_status blz_mat_scale(blz_ctx* c, const blz_block* a, uint64_t rows, uint64_t
   if (!c) return BLZ_INVALID_ARGUMENT;
   if (rows == 0 || cols == 0) return BLZ_OK;
   if (!std::isfinite(k)) return set_err(c, BLZ_INVALID_ARGUMENT, "scale: non-finite constant");
-  blz_cmat ma, mo;
-  if (blz_status st = upload_blocks(c, a, rows, cols, S_CM0, &ma)) return st;
-  if (blz_status st = scratch_cmat(c, S_CM2, rows, cols, &mo)) return st;
-  if (blz_status st = blz_scale_dev(c, &ma, k, &mo)) return st;
-  if (blz_status st = download_blocks(c, &mo, out)) return st;
+  if (blz_status st = elementwise_host(c, 2, a, nullptr, rows, cols, k, out)) return st;
   return latch_status(c);
 }
 
