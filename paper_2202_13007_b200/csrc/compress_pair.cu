@@ -54,17 +54,20 @@ __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64
 //    two's-complement byte of the clamped integer (0x41380000 has a zero low
 //    byte), and every out-of-range t (negative, < 2^20, >= 2^21) clamps to the
 //    correct end;
-//  * near: only for hi inside [0x41380000 + LO, 0x41380000 + HI] (where the
-//    low word is a true fraction), key = frac + m (mod 2^32) is < 2m exactly
-//    when the fraction is within m of 0 or 1; the caller keeps the minimum key.
+//  * near: key = frac + m (mod 2^32) is < 2m exactly when the fraction is within
+//    m of 0 or 1; the caller keeps the minimum key.  Keys of decisions whose high
+//    word lies outside [LO, HI] are kept as well: they can only raise a spurious
+//    "near" (a slower exact recompute), never hide one.  Such a decision cannot
+//    differ from the reference's: the fast value is >= HI + 1/2 (resp. < LO - 1/2),
+//    so with the certified error m < 1/2 the reference rounds to >= HI (<= LO) and
+//    clamps to the same end.  (Magnitudes stay far below the int64 range where the
+//    reference's conversion misbehaves: see the exponent and m_hi guards.)
 template <int LO, int HI>
 __device__ __forceinline__ uint32_t decide_byte(double y, uint32_t mq, uint32_t& kmin) {
   const double t = y + 1572864.5;
   const int hi = (int)hi32(t);
   const int c = min(max(hi, 0x41380000 + LO), 0x41380000 + HI);
-  const bool in = (uint32_t)(hi - (0x41380000 + LO)) <= (uint32_t)(HI - LO);
-  const uint32_t key = lo32(t) + mq;
-  kmin = min(kmin, in ? key : 0xFFFFFFFFu);
+  kmin = min(kmin, lo32(t) + mq);
   return (uint32_t)c & 0xffu;
 }
 
