@@ -5,14 +5,12 @@
 // loaded with coalesced 16-byte accesses into shared memory, combined per lane
 // with exactly the reference's arithmetic, staged and stored coalesced.
 //
-// Exactness of the integer steps without the conversion pipe:
-//  * int8 -> double: __hiloint2double(0x43300000, c ^ 0x80000000) - (2^52 + 2^31)
-//    is exact (one DADD);
-//  * round_half_away (H/block.hpp:61-67) for |x| < 2^50: k = RN_even(x) via
-//    x + 1.5*2^52, fr = x - k (exact, |fr| <= 1/2); at an exact tie (|fr| = 1/2
-//    with the sign of x) the reference rounds away from zero: k + sign(x).
-//    Larger |x| (only possible when s1 + s2 nearly cancels) use the
-//    reference's own truncation sequence (round_half_away in blaz_device.cuh).
+// Exactness of the integer steps:
+//  * int8 -> double: I2F.F64.S8 on a byte lane (exact);
+//  * round_half_away (H/block.hpp:61-67) for |x| < 2^30: k = RN_even(x) is the
+//    low word of x + 1.5*2^52 and fr = x - k is exact.  Exact ties (|fr| = 1/2)
+//    and larger |x| (only when s1 + s2 nearly cancels) send the block's 28
+//    coefficients through the reference's own sequence (clamp_coeff).
 // The s1 + s2 == 0 dense fallback (:36-44) is handed to k_addsub_fallback via
 // the worklist, as before.
 #include "blaz_device.cuh"
@@ -30,20 +28,6 @@ struct __align__(16) WarpRecs {
 
 __device__ __forceinline__ double i8_to_double(int c) {
   return __hiloint2double(0x43300000, (int)((uint32_t)c ^ 0x80000000u)) - 4503601774854144.0;
-}
-
-// clamp_coeff(round_half_away(x)) (H/block.hpp:76-81), exact.
-// k = RN_even(x) (x + 1.5*2^52 - 1.5*2^52); at an exact tie |x - k| = 1/2 the
-// reference rounds away from zero, i.e. to x + copysign(1/2, x), which is an
-// exactly representable integer.  The integer is read from k + 1.5*2^52.
-__device__ __forceinline__ int clamp_coeff_fast(double x) {
-  const uint32_t hx = hi32(x);
-  if ((hx & 0x7FFFFFFFu) >= 0x43100000u) return clamp_coeff(x);  // |x| >= 2^50, inf, NaN
-  const double M = 6755399441055744.0;
-  double k = (x + M) - M;
-  if (fabs(x - k) == 0.5) k = x + __hiloint2double((int)((hx & 0x80000000u) | 0x3FE00000u), 0);
-  const int n = (int)lo32(k + M);
-  return min(max(n, -127), 127);
 }
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
@@ -148,7 +132,8 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
     double os;
     uint32_t ophi;
     uint32_t oc[7];
-    bool fallback = false;
+    bool fallback = false, slow = false;
+    double w1 = 0.0, w2 = 0.0;
     if (s2 == 0.0) {            // (:27)
       os = s1;
       ophi = p1;
@@ -178,8 +163,14 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
       ophi = phi;
       const double a1 = s1 / os;                          // (:51)
       const double a2 = rhs * s2 / os;                    // (:52)
-      const double w1 = a1 / (double)p1 * (double)phi;    // (:53)
-      const double w2 = a2 / (double)p2 * (double)phi;    // (:54)
+      w1 = a1 / (double)p1 * (double)phi;    // (:53)
+      w2 = a2 / (double)p2 * (double)phi;    // (:54)
+      // clamp_coeff(round_half_away(v)) without branches.  |v| <= 127 (|w1| + |w2|)
+      // < 2^30 unless the weights are huge (s1 + s2 nearly cancelling) or NaN; those
+      // blocks take the reference sequence below.  Otherwise round(v) is the
+      // reference's round_half_away exactly: it truncates RZ(v + copysign(1/2, v)),
+      // and RZ never crosses the representable integer floor(|v| + 1/2).
+      slow = !(fabs(w1) + fabs(w2) < 4194304.0);
 #pragma unroll
       for (int w = 0; w < 7; ++w) {
         uint32_t r = 0;
@@ -188,7 +179,8 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
           const double x1 = (double)(int8_t)(uint8_t)(c1[w] >> (8 * q));  // I2F.F64.S8 on a byte lane
           const double x2 = (double)(int8_t)(uint8_t)(c2[w] >> (8 * q));
           const double v = w1 * x1 + w2 * x2;  // (:55-56)
-          r |= (uint32_t)(clamp_coeff_fast(v) & 0xff) << (8 * q);
+          const int n = (int)round(v);
+          r |= (uint32_t)(min(max(n, -127), 127) & 0xff) << (8 * q);
         }
         oc[w] = r;
       }
@@ -199,6 +191,16 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
     ro.phi[lane] = (uint8_t)ophi;
 #pragma unroll
     for (int w = 0; w < 7; ++w) ro.c[lane * 7 + w] = oc[w];
+    if (slow) {  // huge weights: the reference rounding sequence (blaz_device.cuh::clamp_coeff)
+      const uint8_t* b1 = reinterpret_cast<const uint8_t*>(&ra.c[lane * 7]);
+      const uint8_t* b2 = reinterpret_cast<const uint8_t*>(&rb.c[lane * 7]);
+      uint8_t* bo = reinterpret_cast<uint8_t*>(&ro.c[lane * 7]);
+#pragma unroll 1
+      for (int k = 0; k < KEPT; ++k) {
+        const double v = w1 * (double)(int8_t)b1[k] + w2 * (double)(int8_t)b2[k];
+        bo[k] = (uint8_t)clamp_coeff(v);
+      }
+    }
     store_recs(out, t0, nb, lane, ro);
     __syncwarp();
     buf ^= 1;

@@ -168,6 +168,21 @@ def test_identities(port):
     assert blocks_equal(blz.mat_add(ca, b).blocks, blz.mat_add(b, ca).blocks)  # commutes bitwise
 
 
+def test_addsub_rounding_ties_and_large_weights(port):
+    """Exact ties of w1*C1 + w2*C2 (A + A: w = 1/4 for even phi) and huge
+    weights (s1 + s2 nearly cancelling) take the reference rounding sequence."""
+    a = W.smooth_field(96, 128, seed=21).numpy()
+    ca = blz.compress_matrix(a)
+    for other in (ca, blz.mat_scale(ca, 2.0), blz.mat_scale(ca, -0.999999), blz.mat_scale(ca, -1.0000001)):
+        for op, ref in ((blz.mat_add, port.mat_add), (blz.mat_sub, port.mat_sub)):
+            got = op(ca, other).blocks
+            want = ref(ca.blocks, other.blocks)
+            assert blocks_equal(got, want), block_diff_report(got, want)
+    # ties really occur in A + A
+    phis = ca.blocks["scale_factor"]
+    assert np.any(phis % 2 == 0)
+
+
 def test_gemm_fused_mode_tolerance(port):
     a = W.smooth_field(64, 96, seed=3).numpy()
     b = W.smooth_field(96, 40, seed=4).numpy()
