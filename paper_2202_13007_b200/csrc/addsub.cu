@@ -167,22 +167,24 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
       w2 = a2 / (double)p2 * (double)phi;    // (:54)
       // clamp_coeff(round_half_away(v)) without branches.  |v| <= 127 (|w1| + |w2|)
       // < 2^30 unless the weights are huge (s1 + s2 nearly cancelling) or NaN; those
-      // blocks take the reference sequence below.  Otherwise round(v) is the
-      // reference's round_half_away exactly: it truncates RZ(v + copysign(1/2, v)),
-      // and RZ never crosses the representable integer floor(|v| + 1/2).
+      // blocks take the reference sequence below.  Otherwise the reference's
+      // round_half_away is sign(v) * trunc(RZ(|v| + 1/2)) exactly (RZ never crosses
+      // the representable integer floor(|v| + 1/2)), and clamping the magnitude to
+      // 127 before applying the sign is clamp_coeff's [-127, 127].
       slow = !(fabs(w1) + fabs(w2) < 4194304.0);
 #pragma unroll
       for (int w = 0; w < 7; ++w) {
-        uint32_t r = 0;
+        int n[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const double x1 = (double)(int8_t)(uint8_t)(c1[w] >> (8 * q));  // I2F.F64.S8 on a byte lane
           const double x2 = (double)(int8_t)(uint8_t)(c2[w] >> (8 * q));
           const double v = w1 * x1 + w2 * x2;  // (:55-56)
-          const int n = (int)round(v);
-          r |= (uint32_t)(min(max(n, -127), 127) & 0xff) << (8 * q);
+          const int m = min(__double2int_rz(__dadd_rz(fabs(v), 0.5)), 127);
+          const int sg = (int)hi32(v) >> 31;
+          n[q] = (m ^ sg) - sg;
         }
-        oc[w] = r;
+        oc[w] = __byte_perm(__byte_perm(n[0], n[1], 0x0040), __byte_perm(n[2], n[3], 0x0040), 0x5410);
       }
     }
     if (fallback && t < nb) wl[atomicAdd(wl_count, 1ull)] = t;
