@@ -197,7 +197,12 @@ __device__ __forceinline__ double dequant(int c, double phi, double r) {
   return fma(e, r, q);
 }
 
-template <bool SLOPES_ONLY, class Emit>
+// SYM: the basis has the bitwise repeats of the reference's (glibc) basis --
+// row 0 constant, and t(1,7) = -t(1,0), t(2,3) = -t(2,0), t(3,5) = -t(3,2),
+// t(4,4) = -t(4,2) (checked on the host, analyse_basis).  Equal factors give
+// equal (or exactly negated) rounded products, so those products are formed
+// once; every sum keeps the reference's order.
+template <bool SLOPES_ONLY, bool SYM = false, class Emit>
 __device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basis& B, Emit&& emit) {
   const double s = b.s;
   double dq[KEPT];
@@ -214,6 +219,11 @@ __device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basi
     for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : (double)get_coeff(b.c, k) / fphi;
   }
 
+  if (SYM) {  // t(0,u) d(0,j) is the same for every u
+#pragma unroll
+    for (int j = 0; j < BD; ++j) dq[j] = B.t[0] * dq[j];
+  }
+
   double prev[BD];
 #pragma unroll
   for (int u = 0; u < BD; ++u) {
@@ -222,7 +232,7 @@ __device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basi
     double tr[BD];
 #pragma unroll
     for (int j = 0; j < BD; ++j) {
-      double acc = B.t[0 * BD + u] * dq[j];  // d(0,j) = dq[j]
+      double acc = SYM ? dq[j] : B.t[0 * BD + u] * dq[j];  // d(0,j) = dq[j]
       acc += B.t[1 * BD + u] * dq[8 + j];                // d(1,j) = dq[8+j]
       if (j == 0) {
 #pragma unroll
@@ -235,12 +245,29 @@ __device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basi
     }
     // idct2 pass 2 (H/dct.hpp:62-68): x(u,v) = sum_j tmp(u,j) t(j,v)
     double p[BD];
+    if (SYM) {
+      const double p0 = tr[0] * B.t[0];
+      const double q1 = tr[1] * B.t[1 * BD + 0], q2 = tr[2] * B.t[2 * BD + 0];
+      const double q3 = tr[3] * B.t[3 * BD + 2], q4 = tr[4] * B.t[4 * BD + 2];
 #pragma unroll
-    for (int v = 0; v < BD; ++v) {
-      double acc = tr[0] * B.t[0 * BD + v];
+      for (int v = 0; v < BD; ++v) {
+        double acc = p0;
+        acc += v == 0 ? q1 : (v == 7 ? -q1 : tr[1] * B.t[1 * BD + v]);
+        acc += v == 0 ? q2 : (v == 3 ? -q2 : tr[2] * B.t[2 * BD + v]);
+        acc += v == 2 ? q3 : (v == 5 ? -q3 : tr[3] * B.t[3 * BD + v]);
+        acc += v == 2 ? q4 : (v == 4 ? -q4 : tr[4] * B.t[4 * BD + v]);
 #pragma unroll
-      for (int j = 1; j < BD; ++j) acc += tr[j] * B.t[j * BD + v];
-      p[v] = zero ? 0.0 : acc;
+        for (int j = 5; j < BD; ++j) acc += tr[j] * B.t[j * BD + v];
+        p[v] = zero ? 0.0 : acc;
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < BD; ++v) {
+        double acc = tr[0] * B.t[0 * BD + v];
+#pragma unroll
+        for (int j = 1; j < BD; ++j) acc += tr[j] * B.t[j * BD + v];
+        p[v] = zero ? 0.0 : acc;
+      }
     }
     if (SLOPES_ONLY) {
       emit(u, p);
@@ -263,9 +290,9 @@ __device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basi
   }
 }
 
-template <class Emit>
+template <bool SYM = false, class Emit>
 __device__ __forceinline__ void decompress_exact(const RBlock& b, const Basis& B, Emit&& emit) {
-  decompress_rows_impl<false>(b, B, emit);
+  decompress_rows_impl<false, SYM>(b, B, emit);
 }
 
 // dequantize_prediction (H/codec.hpp:150-158) streamed row by row: emit(u, p[8])

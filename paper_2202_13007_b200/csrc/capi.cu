@@ -28,6 +28,7 @@ struct blz_ctx {
   int sm_count = 148;
   int mode = BLZ_MODE_DEFAULT;
   bool fast_ok = false;        // basis admits the verified fast path
+  bool basis_sym = false;      // basis has the reference's repeated magnitudes (decompress sharing)
   blz::FastInfo fast{};
   unsigned long long* d_stats = nullptr;  // [0] compress exact-path blocks, [1] add/sub dense fallbacks
   uint64_t* d_wl = nullptr;               // exact-path worklist: 256 B counter + capacity entries
@@ -82,6 +83,7 @@ blz::LaunchCtx lc(blz_ctx* c) {
   L.wl_count = (unsigned long long*)c->d_wl;
   L.wl = c->d_wl ? c->d_wl + 32 : nullptr;
   L.stats = c->d_stats;
+  L.basis_sym = c->basis_sym;
   return L;
 }
 
@@ -134,6 +136,12 @@ void analyse_basis(blz_ctx* c) {
   // the dropped lo*sigma_i*sigma_j terms are budgeted at 64 u |lo| in E_d
   c->fast_ok = rowabs <= 2.8284271247461903 * (1.0 + 1e-12) && off <= 64.0 * 1.1102230246251565e-16 &&
                std::fabs(c->fast.ss00 - 8.0) < 1e-12;
+  // bitwise repeats the decompress kernel shares products over (blaz_device.cuh, BasisSym)
+  const double* t = c->basis.t;
+  bool sym = t[1 * 8 + 7] == -t[1 * 8 + 0] && t[2 * 8 + 3] == -t[2 * 8 + 0] && t[3 * 8 + 5] == -t[3 * 8 + 2] &&
+             t[4 * 8 + 4] == -t[4 * 8 + 2];
+  for (int k = 1; k < 8; ++k) sym = sym && t[k] == t[0];
+  c->basis_sym = sym;
 }
 
 void* slot(blz_ctx* c, int id, size_t bytes, cudaError_t* e) {

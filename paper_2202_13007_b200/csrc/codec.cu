@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(128) k_compress(const Basis B, const double* _
 
 // Warp-uniform loop (valid lanes predicated) so that the basis streams through
 // uniform registers (LDCU.128) rather than per-thread constant loads.
+template <bool SYM>
 __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, double* __restrict__ dense,
                                                        uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
   const uint64_t nb = in.nb();
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, d
     const RBlock rb = load_block(in, tt);
     const uint64_t r0 = bi * BD, c0 = bj * BD;
     const bool full = valid && aligned && r0 + BD <= crop_rows && c0 + BD <= crop_cols;
-    decompress_exact(rb, B, [&](int u, const double (&row)[BD]) {
+    decompress_exact<SYM>(rb, B, [&](int u, const double (&row)[BD]) {
       if (full) {
         double2* dst = reinterpret_cast<double2*>(dense + (r0 + u) * ld + c0);
 #pragma unroll
@@ -136,8 +137,11 @@ cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in
 
 cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
-  k_decompress<<<grid_for(in.nb(), 128, c.sm_count), 128, 0, c.stream>>>(B, in, dense, ld, crop_rows,
-                                                                        crop_cols);
+  const unsigned g = grid_for(in.nb(), 128, c.sm_count);
+  if (c.basis_sym && !c.exact_only)  // exact mode keeps the plain product-per-term kernel
+    k_decompress<true><<<g, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+  else
+    k_decompress<false><<<g, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
   ++*c.launches;
   return cudaGetLastError();
 }

@@ -23,6 +23,7 @@ struct LaunchCtx {
   uint64_t* wl;                  // exact-path worklist (nb entries)
   unsigned long long* wl_count;  // worklist length
   unsigned long long* stats;     // [0] compress exact-path blocks, [1] add/sub dense-fallback blocks
+  bool basis_sym;                // basis has the reference's repeated magnitudes (blaz_device.cuh, BasisSym)
 };
 
 // compress_pair.cu (verified fast path, two threads per block)

@@ -243,6 +243,26 @@ def test_fast_path_matches_exact_and_oracle(port):
     assert used_exact < 0.25 * n, used_exact
 
 
+def test_decompress_shared_products_match_plain_kernel(port):
+    """The default decompress shares the products of bitwise-repeated basis
+    entries; exact mode runs one product per term.  Both equal the oracle."""
+    tiles = _adversarial_tiles()
+    n = tiles.shape[0]
+    a = W.smooth_field(200, 136, seed=5).numpy()
+    for m in (tiles.reshape(n * 8, 8), a, np.random.default_rng(3).normal(size=(64, 72)) * 1e3):
+        cm = blz.compress_matrix(m)
+        fast = blz.decompress_matrix(cm)
+        ctx = blz.default_context()
+        ctx.set_mode(blz.MODE_EXACT)
+        try:
+            plain = blz.decompress_matrix(cm)
+        finally:
+            ctx.set_mode(blz.MODE_DEFAULT)
+        want = port.decompress_matrix(cm.blocks.reshape(-1), *m.shape)
+        assert np.array_equal(bits(fast), bits(want))
+        assert np.array_equal(bits(plain), bits(want))
+
+
 def test_fast_path_cfg1_sample(port):
     a = W.quadratic_blocks(512, 4096, seed=21)
     ctx = dev.context()
