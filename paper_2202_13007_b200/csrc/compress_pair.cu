@@ -175,27 +175,46 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, 4)
     // ---- mean_slope: serial sum, rows 0-3 then rows 4-7 --------------------
     // (adding |delta| = +0.0 to the never -0.0 running sum is the identity, so
     // summing all entries equals the reference's sum over nonzero entries)
+    // The upper thread runs its half of the sum first so that the lower one can
+    // continue it while the upper computes max |delta| and the count.
     double sum = 0.0, amax = 0.0;
-    int nz = 0;
-    if (h == 1) {
+    if (h == 0) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) sum += fabs(m[k]);
+      sh.sumA[lane] = sum;
       pair_bar(bar);  // B1: upper partial sum ready
-      sum = sh.sumA[lane];
     }
+    // max |delta| (exact), and a zero test: the minimum of (|hi| | lo) over the
+    // cells is 0 iff some delta is +-0 (delta(0,0) = 0 of the upper half is known).
+    // The running maximum is kept as words: one FP64 compare and two 32-bit
+    // selects per cell, the high word's sign cleared by the select's |.|.
+    uint32_t zmin = 0xFFFFFFFFu;
+    float amax_h = 0.0f;
+    uint32_t amax_l = 0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      const double a = fabs(m[k]);
-      sum += a;
-      nz += (a > 0.0);
-      amax = a > amax ? a : amax;
+      const bool gt = fabs(m[k]) > __hiloint2double(__float_as_int(amax_h), (int)amax_l);
+      amax_h = gt ? fabsf(__int_as_float((int)hi32(m[k]))) : amax_h;
+      amax_l = gt ? lo32(m[k]) : amax_l;
+      const uint32_t zk = (hi32(m[k]) & 0x7FFFFFFFu) | lo32(m[k]);
+      zmin = min(zmin, (k == 0 && h == 0) ? 0xFFFFFFFFu : zk);
+    }
+    amax = __hiloint2double(__float_as_int(amax_h), (int)amax_l);
+    int nz = 32 - (h == 0);
+    if (zmin == 0) {  // some zero deltas (rare on real data): count them
+      nz = 0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) nz += fabs(m[k]) > 0.0;
+    }
+    if (h == 1) {
+      pair_bar(bar);  // B1
+      sum = sh.sumA[lane];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) sum += fabs(m[k]);
     }
     sh.amax[h][lane] = amax;
     sh.nz[h][lane] = nz;
-    if (h == 0) {
-      sh.sumA[lane] = sum;
-      pair_bar(bar);  // B1
-    } else {
-      sh.s[lane] = sum;  // the lower thread holds the complete serial sum
-    }
+    if (h == 1) sh.s[lane] = sum;  // the lower thread holds the complete serial sum
     pair_bar(bar);    // B2
     amax = fmax(sh.amax[0][lane], sh.amax[1][lane]);
     nz = sh.nz[0][lane] + sh.nz[1][lane];
