@@ -36,10 +36,15 @@ for line in dis.splitlines():
     if m and infn:
         off2line[int(m.group(1), 16)] = cur
 
-raw = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+raw = subprocess.run(["ncu", "-i", a.rep, "-k", "regex:" + a.kernel, "-c", "1", "--page", "source", "--csv",
+                      "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-h, data = rows[1], rows[2:]
+h = rows[1]
+data = []
+for r in rows[2:]:
+    if r and r[0] == "Kernel Name":
+        break
+    data.append(r)
 ia, iex, iss, isrc = (h.index(k) for k in ("Address", "Instructions Executed",
                                            "Warp Stall Sampling (All Samples)", "Source"))
 base = int(data[0][ia], 16)

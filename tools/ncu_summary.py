@@ -50,7 +50,7 @@ for r in rows[2:]:
         "us": to_us(r, "gpu__time_duration.sum"),
         "read_MB": to_mb(r, "dram__bytes_read.sum"),
         "write_MB": to_mb(r, "dram__bytes_write.sum"),
-        "dram_pct": val(r, "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+        "dram_pct": val(r, "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed") or val(r, "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
         "issue_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "fp64_pct": val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         "alu_pct": val(r, "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
@@ -58,10 +58,10 @@ for r in rows[2:]:
         "regs": int(val(r, "launch__registers_per_thread")),
         "stalls": ", ".join(f"{k}={v:.2f}" for k, v in st[:4]),
     }
-lines = ["| kernel | us | DRAM rd MB | DRAM wr MB | DRAM % | issue % | FP64 % | ALU % | warps % | regs | top stalls |",
+lines = ["| kernel | us | DRAM rd MB | DRAM wr MB | DRAM GB/s | issue % | FP64 % | ALU % | warps % | regs | top stalls |",
          "|---|---|---|---|---|---|---|---|---|---|---|"]
 for k, v in seen.items():
-    lines.append(f"| {k} | {v['us']:.1f} | {v['read_MB']:.1f} | {v['write_MB']:.1f} | {v['dram_pct']:.1f} | "
+    lines.append(f"| {k} | {v['us']:.1f} | {v['read_MB']:.1f} | {v['write_MB']:.1f} | {1000.0 * (v['read_MB'] + v['write_MB']) / max(v['us'], 1e-9):.0f} | "
                  f"{v['issue_pct']:.1f} | {v['fp64_pct']:.1f} | {v['alu_pct']:.1f} | {v['warps_pct']:.1f} | "
                  f"{v['regs']} | {v['stalls']} |")
 out = "\n".join(lines)
