@@ -130,6 +130,17 @@ blz_status blz_decompress_dev(blz_ctx* ctx, const blz_cmat* in, double* dense, u
 blz_status blz_add_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out);
 blz_status blz_sub_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out);
 blz_status blz_scale_dev(blz_ctx* ctx, const blz_cmat* a, double c, const blz_cmat* out);
+/* Fused op chains: the op of blz_add_dev / blz_sub_dev /
+ * blz_scale_dev writing `out`, followed by blz_decompress_dev(out, dense, ld),
+ * in one pass over the operands; results are bitwise those of the two calls.
+ * Replaces the reference sequence mat_add(...) -> decompress_matrix(...)
+ * (H/matrix.hpp:128-151, :113-126). */
+blz_status blz_add_decompress_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out,
+                                  double* dense, uint64_t ld);
+blz_status blz_sub_decompress_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out,
+                                  double* dense, uint64_t ld);
+blz_status blz_scale_decompress_dev(blz_ctx* ctx, const blz_cmat* a, double c, const blz_cmat* out,
+                                    double* dense, uint64_t ld);
 /* Batched mat_dot (H/matrix.hpp:157-173): out[q] = (Ahat Bhat)(i[q], j[q]).
  * i, j, out are device arrays of n entries; indices are validated on device
  * (an out-of-range index latches BLZ_OUT_OF_RANGE). */

@@ -14,6 +14,7 @@
 // The s1 + s2 == 0 dense fallback (:36-44) is handed to k_addsub_fallback via
 // the worklist, as before.
 #include "blaz_device.cuh"
+#include "combine.cuh"
 #include "fastpath.cuh"
 #include "launch.h"
 
@@ -127,66 +128,13 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
       c1[w] = ra.c[lane * 7 + w];
       c2[w] = rb.c[lane * 7 + w];
     }
-    const double rhs = SUB ? -1.0 : 1.0;
-    double of = f1 + rhs * f2;  // (:22)
-    double os;
-    uint32_t ophi;
+    const CombineOut o = combine_record<SUB>(f1, s1, p1, c1, f2, s2, p2, c2);
+    const bool fallback = o.fallback, slow = o.slow;
+    const double of = o.f, os = o.s, w1 = o.w1, w2 = o.w2;
+    const uint32_t ophi = o.phi;
     uint32_t oc[7];
-    bool fallback = false, slow = false;
-    double w1 = 0.0, w2 = 0.0;
-    if (s2 == 0.0) {            // (:27)
-      os = s1;
-      ophi = p1;
 #pragma unroll
-      for (int w = 0; w < 7; ++w) oc[w] = c1[w];
-    } else if (s1 == 0.0) {     // (:28-33)
-      os = s2;
-      ophi = p2;
-#pragma unroll
-      for (int w = 0; w < 7; ++w) {
-        uint32_t r = c2[w];
-        if (SUB) {
-          r = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int c = (int)(int8_t)(uint8_t)(c2[w] >> (8 * q));
-            const int n = (c == -127) ? 127 : -c;
-            r |= (uint32_t)(n & 0xff) << (8 * q);
-          }
-        }
-        oc[w] = r;
-      }
-    } else {
-      os = s1 + s2;             // (:35)
-      fallback = (os == 0.0);   // (:36-44) -> worklist
-      const uint32_t phi = merge_scale_factor(p1, p2);
-      ophi = phi;
-      const double a1 = s1 / os;                          // (:51)
-      const double a2 = rhs * s2 / os;                    // (:52)
-      w1 = a1 / (double)p1 * (double)phi;    // (:53)
-      w2 = a2 / (double)p2 * (double)phi;    // (:54)
-      // clamp_coeff(round_half_away(v)) without branches.  |v| <= 127 (|w1| + |w2|)
-      // < 2^30 unless the weights are huge (s1 + s2 nearly cancelling) or NaN; those
-      // blocks take the reference sequence below.  Otherwise the reference's
-      // round_half_away is sign(v) * trunc(RZ(|v| + 1/2)) exactly (RZ never crosses
-      // the representable integer floor(|v| + 1/2)), and clamping the magnitude to
-      // 127 before applying the sign is clamp_coeff's [-127, 127].
-      slow = !(fabs(w1) + fabs(w2) < 4194304.0);
-#pragma unroll
-      for (int w = 0; w < 7; ++w) {
-        int n[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double x1 = (double)(int8_t)(uint8_t)(c1[w] >> (8 * q));  // I2F.F64.S8 on a byte lane
-          const double x2 = (double)(int8_t)(uint8_t)(c2[w] >> (8 * q));
-          const double v = w1 * x1 + w2 * x2;  // (:55-56)
-          const int m = min(__double2int_rz(__dadd_rz(fabs(v), 0.5)), 127);
-          const int sg = (int)hi32(v) >> 31;
-          n[q] = (m ^ sg) - sg;
-        }
-        oc[w] = __byte_perm(__byte_perm(n[0], n[1], 0x0040), __byte_perm(n[2], n[3], 0x0040), 0x5410);
-      }
-    }
+    for (int w = 0; w < 7; ++w) oc[w] = o.c[w];
     if (fallback && t < nb) wl[atomicAdd(wl_count, 1ull)] = t;
     ro.f[lane] = of;
     ro.s[lane] = os;

@@ -428,6 +428,46 @@ blz_status blz_scale_dev(blz_ctx* c, const blz_cmat* a, double k, const blz_cmat
   return cuda_err(c, blz::launch_scale(lc(c), view(a), k, view(out)), "mat_scale");
 }
 
+// Fused op + decompress: out receives the compressed result
+// (as blz_add_dev / blz_sub_dev / blz_scale_dev) and dense its decompression
+// (as blz_decompress_dev), bitwise equal to the two-call chain.
+static blz_status op_decompress_dev(blz_ctx* c, int op, const blz_cmat* a, const blz_cmat* b, double k,
+                                    const blz_cmat* out, double* dense, uint64_t ld) {
+  const char* what = op == 0 ? "mat_add" : (op == 1 ? "mat_sub" : "mat_scale");
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, what)) return st;
+  if (op != 2) {
+    if (blz_status st = check_cmat(c, b, what)) return st;
+    if (blz_status st = same_dims(c, a->rows, a->cols, b->rows, b->cols, what)) return st;  // H/matrix.hpp:130
+  }
+  if (blz_status st = check_cmat(c, out, what)) return st;
+  if (out->rows != a->rows || out->cols != a->cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": output dimension mismatch");
+  if (ld < a->cols) return set_err(c, BLZ_INVALID_ARGUMENT, "decompress_matrix: ld < cols");
+  const uint64_t nb = a->block_rows * a->block_cols;
+  if (nb == 0) return BLZ_OK;
+  if (op == 2 && !std::isfinite(k)) return set_err(c, BLZ_INVALID_ARGUMENT, "scale: non-finite constant");
+  if (op != 2)
+    if (blz_status st = ensure_worklist(c, nb)) return st;
+  const blz::CMat va = view(a);
+  return cuda_err(c, blz::launch_op_decompress(lc(c), c->basis, op, va, op == 2 ? va : view(b), k, view(out), dense,
+                                               ld, a->rows, a->cols),
+                  what);
+}
+
+blz_status blz_add_decompress_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out,
+                                  double* dense, uint64_t ld) {
+  return op_decompress_dev(c, 0, a, b, 0.0, out, dense, ld);
+}
+blz_status blz_sub_decompress_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out,
+                                  double* dense, uint64_t ld) {
+  return op_decompress_dev(c, 1, a, b, 0.0, out, dense, ld);
+}
+blz_status blz_scale_decompress_dev(blz_ctx* c, const blz_cmat* a, double k, const blz_cmat* out, double* dense,
+                                    uint64_t ld) {
+  return op_decompress_dev(c, 2, a, nullptr, k, out, dense, ld);
+}
+
 blz_status blz_dot_entries_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, const uint64_t* i,
                                const uint64_t* j, uint64_t n, double* out) {
   if (!c) return BLZ_INVALID_ARGUMENT;

@@ -40,6 +40,11 @@ cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in
 cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols);
 // ops.cu
+cudaError_t launch_addsub_fallback(const LaunchCtx& c, const Basis& B, bool sub, const CMat& a, const CMat& b,
+                                   const CMat& out);
+// fused.cu (op followed by decompress; op 0 add, 1 sub, 2 scale)
+cudaError_t launch_op_decompress(const LaunchCtx& c, const Basis& B, int op, const CMat& a, const CMat& b, double k,
+                                 const CMat& out, double* dense, uint64_t ld, uint64_t crop_rows, uint64_t crop_cols);
 cudaError_t launch_addsub(const LaunchCtx& c, const Basis& B, bool sub, const CMat& a, const CMat& b,
                           const CMat& out);
 cudaError_t launch_scale(const LaunchCtx& c, const CMat& a, double k, const CMat& out);

@@ -139,12 +139,19 @@ cudaError_t launch_addsub(const LaunchCtx& c, const Basis& B, bool sub, const CM
   } else {
     k_addsub<false><<<g, 256, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
   }
+  ++*c.launches;
+  return launch_addsub_fallback(c, B, sub, a, b, out);
+}
+
+// Recomputes the worklisted s1 + s2 == 0 blocks (count read on the device).
+cudaError_t launch_addsub_fallback(const LaunchCtx& c, const Basis& B, bool sub, const CMat& a, const CMat& b,
+                                   const CMat& out) {
   const unsigned gf = (unsigned)c.sm_count;
   if (sub)
     k_addsub_fallback<true><<<gf, 128, 0, c.stream>>>(B, a, b, out, c.wl, c.wl_count, c.err, c.stats + 1);
   else
     k_addsub_fallback<false><<<gf, 128, 0, c.stream>>>(B, a, b, out, c.wl, c.wl_count, c.err, c.stats + 1);
-  *c.launches += 2;
+  ++*c.launches;
   return cudaGetLastError();
 }
 

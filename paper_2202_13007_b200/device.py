@@ -19,17 +19,27 @@ def _nb(n: int) -> int:
     return (n + 7) // 8
 
 
-_ctxs: dict[int, Context] = {}
+_ctxs: dict[tuple[int, int], Context] = {}
 
 
 def context(device: int | None = None) -> Context:
+    """The context bound to torch's current stream on `device`.  Each stream gets
+    its own context (own scratch and exact-path worklist), so operations issued
+    on different streams may run concurrently."""
     dev = torch.cuda.current_device() if device is None else device
-    ctx = _ctxs.get(dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    ctx = _ctxs.get((dev, stream))
     if ctx is None:
         ctx = Context(dev)
-        _ctxs[dev] = ctx
-    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+        ctx.set_stream(stream)
+        _ctxs[(dev, stream)] = ctx
     return ctx
+
+
+def contexts(device: int | None = None) -> list[Context]:
+    """All contexts created on `device` (one per stream used)."""
+    dev = torch.cuda.current_device() if device is None else device
+    return [c for (d, _), c in _ctxs.items() if d == dev]
 
 
 class DeviceCMat:
@@ -145,6 +155,44 @@ def scale(a: DeviceCMat, c: float, out: DeviceCMat | None = None) -> DeviceCMat:
     out = out or DeviceCMat(a.rows, a.cols, device=a.buf.device)
     ctx.check(ctx.lib.blz_scale_dev(ctx.handle, a.ref(), C.c_double(c), out.ref()))
     return out
+
+
+def _dense_for(a: DeviceCMat, dense: torch.Tensor | None) -> torch.Tensor:
+    if dense is None:
+        dense = torch.empty((a.rows, a.cols), dtype=torch.float64, device=a.buf.device)
+    assert dense.is_cuda and dense.dtype == torch.float64 and dense.dim() == 2 and dense.stride(1) == 1
+    return dense
+
+
+def add_decompress(a: DeviceCMat, b: DeviceCMat, out: DeviceCMat | None = None,
+                   dense: torch.Tensor | None = None) -> tuple[DeviceCMat, torch.Tensor]:
+    """Fused mat_add -> decompress_matrix: (compressed A+B, its decompression)."""
+    ctx = context(a.buf.device.index)
+    out = out or DeviceCMat(a.rows, a.cols, device=a.buf.device)
+    dense = _dense_for(a, dense)
+    ctx.check(ctx.lib.blz_add_decompress_dev(ctx.handle, a.ref(), b.ref(), out.ref(), _ptr(dense), dense.stride(0)))
+    return out, dense
+
+
+def sub_decompress(a: DeviceCMat, b: DeviceCMat, out: DeviceCMat | None = None,
+                   dense: torch.Tensor | None = None) -> tuple[DeviceCMat, torch.Tensor]:
+    """Fused mat_sub -> decompress_matrix."""
+    ctx = context(a.buf.device.index)
+    out = out or DeviceCMat(a.rows, a.cols, device=a.buf.device)
+    dense = _dense_for(a, dense)
+    ctx.check(ctx.lib.blz_sub_decompress_dev(ctx.handle, a.ref(), b.ref(), out.ref(), _ptr(dense), dense.stride(0)))
+    return out, dense
+
+
+def scale_decompress(a: DeviceCMat, c: float, out: DeviceCMat | None = None,
+                     dense: torch.Tensor | None = None) -> tuple[DeviceCMat, torch.Tensor]:
+    """Fused mat_scale -> decompress_matrix."""
+    ctx = context(a.buf.device.index)
+    out = out or DeviceCMat(a.rows, a.cols, device=a.buf.device)
+    dense = _dense_for(a, dense)
+    ctx.check(ctx.lib.blz_scale_decompress_dev(ctx.handle, a.ref(), C.c_double(c), out.ref(), _ptr(dense),
+                                               dense.stride(0)))
+    return out, dense
 
 
 def dot_entries(a: DeviceCMat, b: DeviceCMat, i: torch.Tensor, j: torch.Tensor) -> torch.Tensor:

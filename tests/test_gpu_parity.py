@@ -371,3 +371,35 @@ def test_blzc_errors_match_reference(golden):
     bad.blocks["slope"][0, 0] = np.inf
     with pytest.raises(blz.IoError, match="write_compressed: non-finite block field"):
         blz.write_compressed(bad)
+
+
+@pytest.mark.parametrize("rows,cols", [(96, 128), (37, 53), (8, 8), (1, 200)])
+def test_fused_op_decompress_matches_chain(port, rows, cols):
+    """add/sub/scale -> decompress in one pass == the two-call chain, bitwise,
+    including the s1 + s2 == 0 fallback, exact ties and huge weights."""
+    a = torch.from_numpy(W.smooth_field(rows, cols, seed=31).numpy()).cuda()
+    b = torch.from_numpy(np.random.default_rng(4).normal(size=(rows, cols))).cuda()
+    ca, cb = dev.compress(a), dev.compress(b)
+    others = [cb, ca, dev.scale(ca, -1.0), dev.scale(ca, -1.0000001), dev.scale(ca, 2.0)]
+    for other in others:
+        for fused, plain in ((dev.add_decompress, dev.add), (dev.sub_decompress, dev.sub)):
+            out, dense = fused(ca, other)
+            ref_c = plain(ca, other)
+            ref_d = dev.decompress(ref_c)
+            dev.sync()
+            hc, hr = out.to_host().blocks, ref_c.to_host().blocks
+            assert blocks_equal(hc, hr), block_diff_report(hc, hr)
+            assert torch.equal(dense.view(torch.int64), ref_d.view(torch.int64))
+    for k in (3.5, -1.0, 0.0, 1e-300):
+        out, dense = dev.scale_decompress(ca, k)
+        ref_c = dev.scale(ca, k)
+        ref_d = dev.decompress(ref_c)
+        dev.sync()
+        assert blocks_equal(out.to_host().blocks, ref_c.to_host().blocks)
+        assert torch.equal(dense.view(torch.int64), ref_d.view(torch.int64))
+    # and against the oracle
+    out, dense = dev.add_decompress(ca, cb)
+    want = port.mat_add(ca.to_host().blocks.reshape(-1), cb.to_host().blocks.reshape(-1))
+    assert blocks_equal(out.to_host().blocks.reshape(-1), want)
+    wd = port.decompress_matrix(want, rows, cols)
+    assert np.array_equal(bits(dense.cpu().numpy()), bits(wd))

@@ -29,7 +29,9 @@ dev.compress(A, cA)
 dev.compress(B, cB)
 fns = {"compress": lambda: dev.compress(A, cA), "decompress": lambda: dev.decompress(cA, out),
        "add": lambda: dev.add(cA, cB, cS), "sub": lambda: dev.sub(cA, cB, cS), "scale": lambda: dev.scale(cA, 3.5, cS),
-       "rowdot": lambda: dev.rowdot(cA, cB), "frobenius": lambda: dev.frobenius(cA, cB)}
+       "rowdot": lambda: dev.rowdot(cA, cB), "frobenius": lambda: dev.frobenius(cA, cB),
+       "add_dec": lambda: dev.add_decompress(cA, cB, cS, out), "sub_dec": lambda: dev.sub_decompress(cA, cB, cS, out),
+       "scale_dec": lambda: dev.scale_decompress(cA, 3.5, cS, out)}
 if any(o.startswith("matmul") for o in args.ops.split(",")):
     scratch = dev.matmul_scratch(cA, cB)
     fns["matmul_exact"] = lambda: dev.matmul(cA, cB, mode=0, out=cS, scratch=scratch)
