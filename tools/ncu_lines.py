@@ -19,6 +19,7 @@ ap.add_argument("kernel")
 ap.add_argument("src")
 ap.add_argument("--blocks", type=float, default=4194304)
 ap.add_argument("--top", type=int, default=30)
+ap.add_argument("--ncu-kernel", help="regex for ncu -k (default: KERNEL_SUBSTR)")
 a = ap.parse_args()
 
 dis = subprocess.run(["nvdisasm", "-gi", a.cubin], capture_output=True, text=True).stdout
@@ -36,7 +37,7 @@ for line in dis.splitlines():
     if m and infn:
         off2line[int(m.group(1), 16)] = cur
 
-raw = subprocess.run(["ncu", "-i", a.rep, "-k", "regex:" + a.kernel, "-c", "1", "--page", "source", "--csv",
+raw = subprocess.run(["ncu", "-i", a.rep, "-k", "regex:" + (a.ncu_kernel or a.kernel), "-c", "1", "--page", "source", "--csv",
                       "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[1]
