@@ -14,6 +14,7 @@
 
 namespace blz {
 
+template <bool SYM>
 __global__ void __launch_bounds__(128) k_dot_entries(const Basis B, CMat a, CMat b,
                                                      const uint64_t* __restrict__ qi,
                                                      const uint64_t* __restrict__ qj, uint64_t n,
@@ -34,13 +35,13 @@ __global__ void __launch_bounds__(128) k_dot_entries(const Basis B, CMat a, CMat
       double arow[BD], bcol[BD];
       const RBlock ba = load_block(a, bi * a.bc + t);
       const RBlock bb = load_block(b, t * b.bc + bj);
-      decompress_exact(ba, B, [&](int u, const double (&row)[BD]) {
+      decompress_exact<SYM>(ba, B, [&](int u, const double (&row)[BD]) {
         if (u == ri) {
 #pragma unroll
           for (int k = 0; k < BD; ++k) arow[k] = row[k];
         }
       });
-      decompress_exact(bb, B, [&](int u, const double (&row)[BD]) {
+      decompress_exact<SYM>(bb, B, [&](int u, const double (&row)[BD]) {
         double v = row[0];
 #pragma unroll
         for (int k = 1; k < BD; ++k) v = (cj == k) ? row[k] : v;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(128) k_dot_entries(const Basis B, CMat a, CMat
 constexpr int RD_WARPS = 2;
 constexpr int RD_SLOT = 74;
 
+template <bool SYM>
 __global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a, CMat b, double* __restrict__ r) {
   __shared__ double P[RD_WARPS][32 * RD_SLOT];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a,
 #pragma unroll
         for (int w = 0; w < 7; ++w) blk.c[w] = cw[w];
         double* slot = S + lane * RD_SLOT;
-        decompress_exact(blk, B, [&](int u, const double (&row)[BD]) {
+        decompress_exact<SYM>(blk, B, [&](int u, const double (&row)[BD]) {
 #pragma unroll
           for (int v = 0; v < BD; ++v) slot[u * 9 + v] = row[v];
         });
@@ -137,7 +139,10 @@ cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a
   if (n == 0) return cudaSuccess;
   const unsigned g = (unsigned)((n + 127) / 128 < (uint64_t)c.sm_count * 16 ? (n + 127) / 128
                                                                              : (uint64_t)c.sm_count * 16);
-  k_dot_entries<<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
+  if (c.basis_sym && !c.exact_only)
+    k_dot_entries<true><<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
+  else
+    k_dot_entries<false><<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
   ++*c.launches;
   return cudaGetLastError();
 }
@@ -147,7 +152,10 @@ cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, con
   const uint64_t want = (groups + RD_WARPS - 1) / RD_WARPS;
   const uint64_t cap = (uint64_t)c.sm_count * 16;
   const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
-  k_rowdot<<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r);
+  if (c.basis_sym && !c.exact_only)  // shared products of the repeated basis entries (blaz_device.cuh)
+    k_rowdot<true><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r);
+  else
+    k_rowdot<false><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r);
   ++*c.launches;
   return cudaGetLastError();
 }
