@@ -15,6 +15,8 @@
 //   dequantize_prediction                    H/codec.hpp:150-158
 //   add / sub / scale / dot / block_mul      H/block_ops.hpp:65-142
 //   reconstruct_rows / reconstruct_cols      H/block_ops.hpp:87-115
+//   write/read_compressed, write/read_dense,
+//   import_csv                               H/io.hpp:93-190
 //   ref::add/sub/scale/dot/mul               H/matrix.hpp:253-300 (dense baselines)
 //
 // Every compressed-domain result is computed on the GPU (one process-wide
@@ -25,10 +27,12 @@
 #define BLAZ_DROPIN_BLAZ_HPP
 
 #include <array>
+#include <charconv>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <istream>
 #include <iterator>
 #include <mutex>
@@ -309,6 +313,97 @@ inline compressed_matrix read_compressed(std::istream& in) {
     gpu::check(blz_read_compressed(gpu::context(), bytes.data(), bytes.size(), &rows, &cols,
                                    gpu::raw(cm.blocks.data()), cm.blocks.size()));
     return cm;
+}
+
+// ---- dense container and CSV import (H/io.hpp:135-190), host byte formatting ------
+// "BLZD", version 1, u32 rows, u32 cols (little endian), then rows*cols binary64.
+namespace detail {
+
+inline void put_le(std::string& out, std::uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) out.push_back(char((v >> (8 * i)) & 0xff));
+}
+
+inline std::uint64_t get_le(const unsigned char* p, int bytes) {
+    std::uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= std::uint64_t(p[i]) << (8 * i);
+    return v;
+}
+
+}  // namespace detail
+
+inline std::size_t write_dense(const dense_matrix& m, std::ostream& out) {
+    std::string bytes;
+    bytes.reserve(13 + m.values.size() * 8);
+    bytes.append("BLZD", 4);
+    bytes.push_back(char(1));
+    detail::put_le(bytes, std::uint32_t(m.rows), 4);
+    detail::put_le(bytes, std::uint32_t(m.cols), 4);
+    for (double v : m.values) {
+        std::uint64_t u;
+        std::memcpy(&u, &v, 8);
+        detail::put_le(bytes, u, 8);
+    }
+    out.write(bytes.data(), std::streamsize(bytes.size()));
+    if (!out) throw io_error("write_dense: write failed");
+    return bytes.size();
+}
+
+inline dense_matrix read_dense(std::istream& in) {
+    unsigned char h[13];
+    in.read(reinterpret_cast<char*>(h), 13);
+    if (in.gcount() != 13) throw io_error("dense matrix: truncated header");
+    if (std::memcmp(h, "BLZD", 4) != 0) throw io_error("dense matrix: magic mismatch (not a dense matrix file)");
+    if (h[4] != 1) throw io_error("dense matrix: unsupported version " + std::to_string(h[4]));
+    const std::size_t rows = detail::get_le(h + 5, 4), cols = detail::get_le(h + 9, 4);
+    if (rows == 0 || cols == 0) throw io_error("dense matrix: zero dimension in header");
+    dense_matrix m(rows, cols);
+    std::vector<unsigned char> buf(m.values.size() * 8);
+    in.read(reinterpret_cast<char*>(buf.data()), std::streamsize(buf.size()));
+    if (std::size_t(in.gcount()) != buf.size()) throw io_error("dense matrix: truncated payload");
+    for (std::size_t k = 0; k < m.values.size(); ++k) {
+        const std::uint64_t u = detail::get_le(buf.data() + 8 * k, 8);
+        std::memcpy(&m.values[k], &u, 8);
+    }
+    return m;
+}
+
+// One matrix row per line, comma-separated decimal cells ('.' separator, blanks
+// around cells allowed); every row must have the same number of cells.
+inline dense_matrix import_csv(std::istream& in) {
+    std::vector<double> values;
+    std::size_t rows = 0, cols = 0;
+    std::string line;
+    while (std::getline(in, line)) {
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        if (line.empty() && in.peek() == std::char_traits<char>::eof()) break;
+        ++rows;
+        std::size_t cells = 0, pos = 0;
+        for (;;) {
+            const std::size_t comma = line.find(',', pos);
+            const char* b = line.data() + pos;
+            const char* e = line.data() + (comma == std::string::npos ? line.size() : comma);
+            while (b != e && (*b == ' ' || *b == '\t')) ++b;
+            while (e != b && (e[-1] == ' ' || e[-1] == '\t')) --e;
+            double v = 0.0;
+            const auto [ptr, ec] = std::from_chars(b, e, v);
+            if (ec != std::errc{} || ptr != e || b == e)
+                throw io_error("csv: non-numeric cell at row " + std::to_string(rows) + ", column " +
+                               std::to_string(cells + 1));
+            values.push_back(v);
+            ++cells;
+            if (comma == std::string::npos) break;
+            pos = comma + 1;
+        }
+        if (rows == 1)
+            cols = cells;
+        else if (cells != cols)
+            throw io_error("csv: row " + std::to_string(rows) + " has " + std::to_string(cells) + " cells, expected " +
+                           std::to_string(cols));
+    }
+    if (rows == 0) throw io_error("csv: empty input");
+    dense_matrix m(rows, cols);
+    m.values = std::move(values);
+    return m;
 }
 
 // ---- uncompressed baselines (H/matrix.hpp:253-300), CPU ---------------------------
