@@ -17,6 +17,8 @@
 //   reconstruct_rows / reconstruct_cols      H/block_ops.hpp:87-115
 //   write/read_compressed, write/read_dense,
 //   import_csv                               H/io.hpp:93-190
+//   gen_matrix, mean_relative_error, accuracy_suite, bench_suite, ...
+//                                            H/bench.hpp (blaz/harness.hpp)
 //   ref::add/sub/scale/dot/mul               H/matrix.hpp:253-300 (dense baselines)
 //
 // Every compressed-domain result is computed on the GPU (one process-wide
@@ -455,5 +457,7 @@ inline dense_matrix mul(const dense_matrix& a, const dense_matrix& b) {
 }  // namespace ref
 
 }  // namespace blaz
+
+#include "harness.hpp"  // H/bench.hpp: the evaluation harness, as in the reference's umbrella header
 
 #endif  // BLAZ_DROPIN_BLAZ_HPP

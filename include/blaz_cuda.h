@@ -200,6 +200,18 @@ blz_status blz_decompress_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, 
 /* dequantize_prediction (H/codec.hpp:150-158): the 8x8 slope grid of each block. */
 blz_status blz_dequantize_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, double* tiles);
 
+/* ---- evaluation harness --------------------------------
+ * mean_relative_error (H/bench.hpp:67-84): mean of |(cand - ref) / ref| over
+ * the entries with |ref| >= 1e-12 (serial sum in index order, as the
+ * reference), and the count of excluded entries.  _dev: device arrays of n
+ * entries, results written to device memory; host variant: host matrices with
+ * the reference's dimension check ("mean_relative_error: dimension mismatch"). */
+blz_status blz_mean_relative_error_dev(blz_ctx* ctx, const double* ref, const double* cand, uint64_t n,
+                                       double* mean, uint64_t* excluded);
+blz_status blz_mean_relative_error(blz_ctx* ctx, const double* ref, uint64_t ref_rows, uint64_t ref_cols,
+                                   const double* cand, uint64_t cand_rows, uint64_t cand_cols, double* mean,
+                                   uint64_t* excluded);
+
 /* ---- .blzc container (H/io.hpp:93-134) --------------------------------------- */
 /* 13-byte header ("BLZC", version 1, rows, cols as LE u32) + 45-byte records
  * (f, s LE binary64, scale byte, 28 coefficients) in row-major block order. */

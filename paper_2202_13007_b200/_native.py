@@ -81,6 +81,8 @@ SIGNATURES = {
     "blz_add_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_sub_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_scale_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
+    "blz_mean_relative_error_dev": (_ST, [_P, _P, _P, _U64, _P, _P]),
+    "blz_mean_relative_error": (_ST, [_P, _P, _U64, _U64, _P, _U64, _U64, _P, _P]),
     "blz_add_decompress_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _U64]),
     "blz_sub_decompress_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _U64]),
     "blz_scale_decompress_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat), _P, _U64]),

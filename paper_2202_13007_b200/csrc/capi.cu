@@ -790,6 +790,33 @@ blz_status blz_mat_dot(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac,
   return latch_status(c);
 }
 
+// ---- evaluation harness (H/bench.hpp:67-84) ------------------------------------
+blz_status blz_mean_relative_error_dev(blz_ctx* c, const double* ref, const double* cand, uint64_t n, double* mean,
+                                       uint64_t* excluded) {
+  if (!c || !mean || !excluded) return BLZ_INVALID_ARGUMENT;
+  return cuda_err(c, blz::launch_mean_rel_error(lc(c), ref, cand, n, mean, (unsigned long long*)excluded),
+                  "mean_relative_error");
+}
+
+blz_status blz_mean_relative_error(blz_ctx* c, const double* ref, uint64_t rr, uint64_t rc, const double* cand,
+                                   uint64_t cr, uint64_t cc, double* mean, uint64_t* excluded) {
+  if (!c || !mean || !excluded) return BLZ_INVALID_ARGUMENT;
+  if (rr != cr || rc != cc) return set_err(c, BLZ_INVALID_ARGUMENT, "mean_relative_error: dimension mismatch");
+  const uint64_t n = rr * rc;
+  cudaError_t e;
+  double* d = (double*)slot(c, S_IN0, (2 * n + 2) * sizeof(double), &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  if (n) {
+    BLZ_CUDA(c, cudaMemcpyAsync(d, ref, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+    BLZ_CUDA(c, cudaMemcpyAsync(d + n, cand, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+  }
+  double* res = d + 2 * n;
+  if (blz_status st = blz_mean_relative_error_dev(c, d, d + n, n, res, (uint64_t*)(res + 1))) return st;
+  BLZ_CUDA(c, cudaMemcpyAsync(mean, res, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  BLZ_CUDA(c, cudaMemcpyAsync(excluded, res + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  return latch_status(c);
+}
+
 static blz_status mat_mul_host(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac, const blz_block* b,
                                uint64_t br, uint64_t bc, blz_block* out_c, double* out_d) {
   if (!c) return BLZ_INVALID_ARGUMENT;

@@ -61,6 +61,9 @@ cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out);
 cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r);
 cudaError_t launch_sum(const LaunchCtx& c, const double* v, uint64_t n, double* out);
+// harness.cu (evaluation-harness reduction)
+cudaError_t launch_mean_rel_error(const LaunchCtx& c, const double* ref, const double* cand, uint64_t n,
+                                  double* mean, unsigned long long* excluded);
 // gemm.cu
 cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t lda, const double* Bm,
                         uint64_t ldb, double* Cm, uint64_t ldc, uint64_t M, uint64_t N, uint64_t K);

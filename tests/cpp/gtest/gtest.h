@@ -94,6 +94,7 @@ inline int run_all() {
     mini_gtest::Reporter(__FILE__, __LINE__, what, fatal)
 
 #define EXPECT_TRUE(c) MG_CHECK((c), "EXPECT_TRUE(" #c ")", false)
+#define FAIL() MG_CHECK(false, "FAIL()", true)
 #define ASSERT_TRUE(c) MG_CHECK((c), "ASSERT_TRUE(" #c ")", true)
 #define EXPECT_EQ(a, b) MG_CHECK((a) == (b), "EXPECT_EQ(" #a ", " #b ")", false)
 #define ASSERT_EQ(a, b) MG_CHECK((a) == (b), "ASSERT_EQ(" #a ", " #b ")", true)

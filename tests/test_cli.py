@@ -52,7 +52,9 @@ def test_usage_errors(tmp_path):
     assert run("frobnicate")[0] == 1
     assert run("compress")[0] == 1  # missing input and output
     assert run("--bogus", "info", "x")[0] == 1
-    assert run("accuracy", "-o", str(tmp_path / "a.csv"))[0] == 1
+    assert run("accuracy", "-n", "1", "-o", str(tmp_path / "a.csv"))[0] == 3
+    assert run("bench", "--repeats", "4", "-o", str(tmp_path / "b.csv"))[0] == 3
+    assert run("bench", "--ops", "frob", "-o", str(tmp_path / "b.csv"))[0] == 3
     code, out, _ = run("--help")
     assert code == 0 and "compress" in out
 
@@ -125,6 +127,14 @@ def test_matrix_commands_match_reference(golden, tmp_path, n):
     o = tmp_path / "mul.blzc"
     assert run("matmul", str(ca), str(cbt), "-o", str(o))[0] == 0
     assert open(o, "rb").read() == blzc_bytes(g("mul"), rows, rows)
+    if n == 3:  # the harness subcommands (GPU mean_relative_error, timing)
+        acc = tmp_path / "acc.csv"
+        assert run("accuracy", "-n", "24", "-o", str(acc))[0] == 0
+        lines = acc.read_text().splitlines()
+        assert lines[0] == "op,lhs,rhs,n,error,excluded" and len(lines) == 64
+        bench = tmp_path / "bench.csv"
+        assert run("bench", "--sizes", "16", "--ops", "add,compress", "-o", str(bench))[0] == 0
+        assert bench.read_text().splitlines()[0] == "op,n,variant,seconds"
     code, out, _ = run("info", str(ca))
     assert code == 0 and f"dimensions:       {rows} x {cols}" in out
     # errors: dimension mismatch -> 3, out-of-range dot -> 3, corrupt file -> 2

@@ -403,3 +403,30 @@ def test_fused_op_decompress_matches_chain(port, rows, cols):
     assert blocks_equal(out.to_host().blocks.reshape(-1), want)
     wd = port.decompress_matrix(want, rows, cols)
     assert np.array_equal(bits(dense.cpu().numpy()), bits(wd))
+
+
+def test_mean_relative_error_serial_order():
+    """blz_mean_relative_error (H/bench.hpp:67-84) == the reference's serial loop, bitwise."""
+    import ctypes as C
+    rng = np.random.default_rng(8)
+    n = 5000
+    ref = rng.normal(size=n) * 10.0 ** rng.integers(-14, 3, size=n)
+    ref[::17] = 0.0
+    cand = ref * (1.0 + rng.normal(size=n) * 1e-6) + rng.normal(size=n) * 1e-9
+    total, kept = 0.0, 0
+    for r, c in zip(ref.tolist(), cand.tolist()):
+        if abs(r) < 1e-12:
+            continue
+        total += abs((c - r) / r)
+        kept += 1
+    want = total / kept
+    ctx = blz.default_context()
+    mean, exc = C.c_double(), C.c_uint64()
+    a, b = np.ascontiguousarray(ref), np.ascontiguousarray(cand)
+    ctx.check(ctx.lib.blz_mean_relative_error(ctx.handle, a.ctypes.data, 50, 100, b.ctypes.data, 50, 100,
+                                              C.byref(mean), C.byref(exc)))
+    assert np.float64(mean.value).view(np.uint64) == np.float64(want).view(np.uint64)
+    assert exc.value == n - kept
+    with pytest.raises(blz.InvalidArgument, match="dimension mismatch"):
+        ctx.check(ctx.lib.blz_mean_relative_error(ctx.handle, a.ctypes.data, 50, 100, b.ctypes.data, 100, 50,
+                                                  C.byref(mean), C.byref(exc)))

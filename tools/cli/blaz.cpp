@@ -5,8 +5,7 @@
 // error, 3 dimension/argument error.  Every matrix operation goes through the
 // drop-in header include/blaz/blaz.hpp, i.e. runs on the B200; the argument
 // parser is a small hand-written one (the reference uses CLI11, absent here).
-// The evaluation-harness subcommands (accuracy, bench; H/bench.hpp) are not
-// part of this build and report a usage error.
+// accuracy / bench run the evaluation harness of the drop-in (blaz/harness.hpp).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -40,7 +39,9 @@ const char* kUsage =
     "  sub <a.blzc> <b.blzc> -o out.blzc\n"
     "  scale <in.blzc> <c> -o out.blzc\n"
     "  dot <a.blzc> <b.blzc> <i> <j>\n"
-    "  matmul <a.blzc> <b.blzc> -o out.blzc\n";
+    "  matmul <a.blzc> <b.blzc> -o out.blzc\n"
+    "  accuracy [-n N] -o out.csv                  the accuracy table (default n 512)\n"
+    "  bench [--sizes a,b] [--ops x,y] [--repeats R] -o out.csv\n";
 
 // Parsed command line: global flags, the subcommand, its positionals and -o.
 struct Args {
@@ -48,6 +49,8 @@ struct Args {
     unsigned threads = 1;
     std::string cmd, output;
     std::vector<std::string> pos;
+    std::string size = "512", sizes = "80,400,1000,2000", ops = "add,scale,dot,matmul,compress,decompress",
+                repeats = "5";
 };
 
 Args parse(int argc, char** argv) {
@@ -68,6 +71,14 @@ Args parse(int argc, char** argv) {
             a.threads = unsigned(n);
         } else if (t == "-o" || t == "--output") {
             a.output = value("--output");
+        } else if (t == "-n" || t == "--size") {
+            a.size = value("--size");
+        } else if (t == "--sizes") {
+            a.sizes = value("--sizes");
+        } else if (t == "--ops") {
+            a.ops = value("--ops");
+        } else if (t == "--repeats") {
+            a.repeats = value("--repeats");
         } else if (t.rfind("--output=", 0) == 0) {
             a.output = t.substr(9);
         } else if (t.size() > 1 && t[0] == '-' && !(t.size() > 1 && (std::isdigit((unsigned char)t[1]) || t[1] == '.'))) {
@@ -132,33 +143,49 @@ blaz::compressed_matrix load_compressed(const std::string& path) {
     return blaz::read_compressed(in);
 }
 
-// The paper's six test surfaces (section 4), sampled on [-2,2]^2 with
-// nodes -2 + 4j/(n-1): M(i,j) = f(x_j, y_i).
-// (each expression in the reference's evaluation order, H/bench.hpp:26-36)
-double surface(int id, double x, double y) {
-    switch (id) {
-        case 1: return x * y;
-        case 2: return x * y / (1.0 + x * x + y * y);
-        case 3: return x * x - y;
-        case 4: return (x * x) * (y * y);
-        case 5: return std::cos(std::sqrt(x * x + y * y));
-        default: return std::cos(x * x + y * y) * std::exp(-0.1 * (x * x + y * y));
-    }
-}
-
 blaz::dense_matrix gen(const std::string& fn, const std::string& ns) {
-    if (fn.size() != 2 || fn[0] != 'f' || fn[1] < '1' || fn[1] > '6')
-        throw argument_error("unknown test function '" + fn + "' (expected f1..f6)");
+    const blaz::test_function* f = blaz::find_test_function(fn);
+    if (!f) throw argument_error("unknown test function '" + fn + "' (expected f1..f6)");
     char* end = nullptr;
     const unsigned long long n = std::strtoull(ns.c_str(), &end, 10);
     if (ns.empty() || *end) throw usage_error("gen: n is not a number: " + ns);
     if (n < 2) throw argument_error("n must be at least 2");
-    std::vector<double> nodes(n);
-    for (std::size_t j = 0; j < n; ++j) nodes[j] = -2.0 + 4.0 * double(j) / double(n - 1);
-    blaz::dense_matrix m(n, n);
-    for (std::size_t i = 0; i < n; ++i)
-        for (std::size_t j = 0; j < n; ++j) m(i, j) = surface(fn[1] - '0', nodes[j], nodes[i]);
-    return m;
+    return blaz::gen_matrix(*f, n);
+}
+
+std::vector<std::size_t> parse_sizes(const std::string& csv) {
+    std::vector<std::size_t> out;
+    std::size_t pos = 0;
+    while (pos <= csv.size()) {
+        const std::size_t comma = csv.find(',', pos);
+        const std::string tok = csv.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+        char* end = nullptr;
+        const unsigned long v = std::strtoul(tok.c_str(), &end, 10);
+        if (tok.empty() || *end || v < 2) throw argument_error("bad size '" + tok + "'");
+        out.push_back(v);
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+    }
+    return out;
+}
+
+std::vector<blaz::bench_op> parse_ops(const std::string& csv) {
+    std::vector<blaz::bench_op> out;
+    std::size_t pos = 0;
+    while (pos <= csv.size()) {
+        const std::size_t comma = csv.find(',', pos);
+        const std::string tok = csv.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+        bool found = false;
+        for (const blaz::bench_op op : blaz::all_bench_ops())
+            if (tok == blaz::name_of(op)) {
+                out.push_back(op);
+                found = true;
+            }
+        if (!found) throw argument_error("unknown op '" + tok + "' (expected add,scale,dot,matmul,compress,decompress)");
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+    }
+    return out;
 }
 
 double parse_double(const std::string& s, const char* what) {
@@ -217,8 +244,24 @@ int run(const Args& a) {
         need(a, 2, true);
         const blaz::compressed_matrix x = load_compressed(a.pos[0]), y = load_compressed(a.pos[1]);
         save_c(blaz::mat_mul(x, y, th));
-    } else if (a.cmd == "accuracy" || a.cmd == "bench") {
-        throw usage_error(a.cmd + ": the evaluation harness (H/bench.hpp) is not part of this build");
+    } else if (a.cmd == "accuracy") {
+        need(a, 0, true);
+        char* end = nullptr;
+        const unsigned long long n = std::strtoull(a.size.c_str(), &end, 10);
+        if (a.size.empty() || *end) throw usage_error("--size: not a number: " + a.size);
+        if (n < 2) throw argument_error("size must be at least 2");
+        const auto rows = blaz::accuracy_suite(n, th);
+        write_atomically(a.output, a.force, [&](std::ostream& o) { blaz::write_accuracy_csv(rows, o); });
+    } else if (a.cmd == "bench") {
+        need(a, 0, true);
+        const auto sizes = parse_sizes(a.sizes);
+        const auto ops = parse_ops(a.ops);
+        char* end = nullptr;
+        const long r = std::strtol(a.repeats.c_str(), &end, 10);
+        if (a.repeats.empty() || *end) throw usage_error("--repeats: not a number: " + a.repeats);
+        if (r < 5) throw argument_error("repeats must be at least 5");
+        const auto rows = blaz::bench_suite(sizes, ops, int(r), th);
+        write_atomically(a.output, a.force, [&](std::ostream& o) { blaz::write_bench_csv(rows, o); });
     } else {
         throw usage_error("unknown subcommand '" + a.cmd + "'");
     }
