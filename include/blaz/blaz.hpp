@@ -15,6 +15,9 @@
 //   dequantize_prediction                    H/codec.hpp:150-158
 //   add / sub / scale / dot / block_mul      H/block_ops.hpp:65-142
 //   reconstruct_rows / reconstruct_cols      H/block_ops.hpp:87-115
+//   normalize / denormalize / mean_slope / predict / quantize_coeffs,
+//   dct2 / idct2 (stage functions)           H/codec.hpp:12-125, H/dct.hpp:14-70
+//   round_half_away / clamp_index / clamp_coeff / all_finite  H/block.hpp:61-87
 //   write/read_compressed, write/read_dense,
 //   import_csv                               H/io.hpp:93-190
 //   gen_matrix, mean_relative_error, accuracy_suite, bench_suite, ...
@@ -220,6 +223,119 @@ inline dense_matrix mat_mul_dense(const compressed_matrix& a, const compressed_m
                                  gpu::raw(b.blocks.data()), b.rows, b.cols, out.values.data(), threads));
     return out;
 }
+
+// ---- scalar helpers of the codec (H/block.hpp:61-87) ---------------------------
+// Reference semantics, including the x86 conversion of out-of-range values to
+// INT64_MIN inside round_half_away; used by callers and by slope_quantizer.
+inline double round_half_away(double x) {
+    const double t = (x >= -9223372036854775808.0 && x < 9223372036854775808.0)
+                         ? double(static_cast<long long>(x))
+                         : -9223372036854775808.0;
+    const double frac = x - t;
+    if (frac >= 0.5) return t + 1.0;
+    if (frac <= -0.5) return t - 1.0;
+    return t;
+}
+
+inline int clamp_index(double x) {
+    const double r = round_half_away(x);
+    return r <= 0.0 ? 0 : (r >= 255.0 ? 255 : int(r));
+}
+
+inline std::int8_t clamp_coeff(double x) {
+    const double r = round_half_away(x);
+    return r <= -127.0 ? std::int8_t(-127) : (r >= 127.0 ? std::int8_t(127) : std::int8_t(r));
+}
+
+inline bool all_finite(const block8& b) {
+    for (double v : b.a)
+        if (!std::isfinite(v)) return false;
+    return true;
+}
+
+// ---- stage functions (H/codec.hpp:12-125, H/dct.hpp:14-70), on the GPU ----------
+struct normalization {
+    double first = 0.0;
+    block8 deltas;
+};
+
+struct slope_quantizer {
+    double lo = 0.0;
+    double step = 0.0;
+    static constexpr int levels = 256;
+    int encode(double v) const { return step == 0.0 ? 0 : clamp_index((v - lo) / step); }
+    double decode(int k) const { return lo + k * step; }
+};
+
+struct prediction_block {
+    std::array<std::uint8_t, block_cells> indices{};
+    block8 snapped;
+};
+
+struct prediction_result {
+    prediction_block prediction;
+    slope_quantizer quantizer;
+};
+
+struct coeff_quantization {
+    std::uint8_t scale_factor = 1;
+    std::array<std::int8_t, kept_coeff_count> coeffs{};
+};
+
+inline normalization normalize(const block8& m) {
+    normalization out;
+    gpu::check(blz_normalize_blocks(gpu::context(), m.a.data(), 1, &out.first, out.deltas.a.data()));
+    return out;
+}
+
+inline block8 denormalize(double first, const block8& deltas) {
+    block8 out;
+    gpu::check(blz_denormalize_blocks(gpu::context(), &first, deltas.a.data(), 1, out.a.data()));
+    return out;
+}
+
+inline double mean_slope(const block8& deltas) {
+    double s = 0.0;
+    gpu::check(blz_mean_slope_blocks(gpu::context(), deltas.a.data(), 1, &s));
+    return s;
+}
+
+inline prediction_result predict(const block8& slopes, double slope_mean) {
+    prediction_result out;
+    gpu::check(blz_predict_blocks(gpu::context(), slopes.a.data(), &slope_mean, 1, out.prediction.indices.data(),
+                                  out.prediction.snapped.a.data(), &out.quantizer.lo, &out.quantizer.step));
+    return out;
+}
+
+inline coeff_quantization quantize_coeffs(const block8& d) {
+    coeff_quantization out;
+    gpu::check(blz_quantize_coeffs_blocks(gpu::context(), d.a.data(), 1, &out.scale_factor, out.coeffs.data()));
+    return out;
+}
+
+inline block8 dct2(const block8& x) {
+    block8 out;
+    gpu::check(blz_dct2_blocks(gpu::context(), x.a.data(), 1, out.a.data()));
+    return out;
+}
+
+inline block8 idct2(const block8& d) {
+    block8 out;
+    gpu::check(blz_idct2_blocks(gpu::context(), d.a.data(), 1, out.a.data()));
+    return out;
+}
+
+namespace detail {
+// The context's uploaded basis (H/dct.hpp:14-27, computed on the host with glibc).
+inline const block8& dct_basis() {
+    static const block8 t = [] {
+        block8 m;
+        gpu::check(blz_ctx_basis(gpu::context(), m.a.data()));
+        return m;
+    }();
+    return t;
+}
+}  // namespace detail
 
 // ---- block level (batched calls of one block) ----------------------------------
 inline compressed_block compress_block(const block8& m) {

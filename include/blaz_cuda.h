@@ -200,6 +200,25 @@ blz_status blz_decompress_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, 
 /* dequantize_prediction (H/codec.hpp:150-158): the 8x8 slope grid of each block. */
 blz_status blz_dequantize_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, double* tiles);
 
+/* ---- stage functions of the codec, batched ---------------
+ * Host arrays of n blocks (64 doubles each, row-major), computed on the GPU one
+ * thread per block in the reference's order:
+ *   normalize (H/codec.hpp:20-32): first[n], deltas[n*64]; non-finite input
+ *     -> BLZ_INVALID_ARGUMENT "normalize: non-finite input"
+ *   denormalize (:35-44), mean_slope (:47-57)
+ *   predict (:61-98): indices[n*64], snapped[n*64], quantizer lo[n], step[n];
+ *     slope_mean <= 0 -> "predict: mean slope must be positive"
+ *   quantize_coeffs (:108-125): scale[n], coeffs[n*28] (keep-set order)
+ *   dct2 / idct2 (H/dct.hpp:32-70) with the context's basis */
+blz_status blz_normalize_blocks(blz_ctx* ctx, const double* m, uint64_t n, double* first, double* deltas);
+blz_status blz_denormalize_blocks(blz_ctx* ctx, const double* first, const double* deltas, uint64_t n, double* m);
+blz_status blz_mean_slope_blocks(blz_ctx* ctx, const double* deltas, uint64_t n, double* s);
+blz_status blz_predict_blocks(blz_ctx* ctx, const double* slopes, const double* slope_mean, uint64_t n,
+                              uint8_t* indices, double* snapped, double* lo, double* step);
+blz_status blz_quantize_coeffs_blocks(blz_ctx* ctx, const double* d, uint64_t n, uint8_t* scale, int8_t* coeffs);
+blz_status blz_dct2_blocks(blz_ctx* ctx, const double* x, uint64_t n, double* d);
+blz_status blz_idct2_blocks(blz_ctx* ctx, const double* d, uint64_t n, double* x);
+
 /* ---- evaluation harness --------------------------------
  * mean_relative_error (H/bench.hpp:67-84): mean of |(cand - ref) / ref| over
  * the entries with |ref| >= 1e-12 (serial sum in index order, as the

@@ -81,6 +81,13 @@ SIGNATURES = {
     "blz_add_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_sub_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_scale_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
+    "blz_normalize_blocks": (_ST, [_P, _P, _U64, _P, _P]),
+    "blz_denormalize_blocks": (_ST, [_P, _P, _P, _U64, _P]),
+    "blz_mean_slope_blocks": (_ST, [_P, _P, _U64, _P]),
+    "blz_predict_blocks": (_ST, [_P, _P, _P, _U64, _P, _P, _P, _P]),
+    "blz_quantize_coeffs_blocks": (_ST, [_P, _P, _U64, _P, _P]),
+    "blz_dct2_blocks": (_ST, [_P, _P, _U64, _P]),
+    "blz_idct2_blocks": (_ST, [_P, _P, _U64, _P]),
     "blz_mean_relative_error_dev": (_ST, [_P, _P, _P, _U64, _P, _P]),
     "blz_mean_relative_error": (_ST, [_P, _P, _U64, _U64, _P, _U64, _U64, _P, _P]),
     "blz_add_decompress_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _U64]),

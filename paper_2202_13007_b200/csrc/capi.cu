@@ -790,6 +790,77 @@ blz_status blz_mat_dot(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac,
   return latch_status(c);
 }
 
+// ---- stage functions (H/codec.hpp, H/dct.hpp), batched over n blocks ------------
+// Host arrays in and out; staged through one scratch slot.  The kernels latch
+// the reference's errors (normalize: non-finite input; predict: mean slope).
+static blz_status stage_call(blz_ctx* c, int stage, const double* in0, uint64_t in0_per, const double* in1,
+                             uint64_t in1_per, uint64_t n, double* out0, uint64_t out0_per, double* out1,
+                             uint64_t out1_per, double* out2, uint64_t out2_per, void* out3, uint64_t out3_bytes) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (n == 0) return BLZ_OK;
+  const uint64_t doubles = n * (in0_per + in1_per + out0_per + out1_per + out2_per) + (n * out3_bytes + 7) / 8;
+  cudaError_t e;
+  double* d = (double*)slot(c, S_IN0, doubles * sizeof(double) + 64, &e);
+  if (!d) return cuda_err(c, e, "scratch allocation");
+  double* d_in0 = d;
+  double* d_in1 = d_in0 + n * in0_per;
+  double* d_out0 = d_in1 + n * in1_per;
+  double* d_out1 = d_out0 + n * out0_per;
+  double* d_out2 = d_out1 + n * out1_per;
+  void* d_out3 = d_out2 + n * out2_per;
+  BLZ_CUDA(c, cudaMemcpyAsync(d_in0, in0, n * in0_per * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+  if (in1_per)
+    BLZ_CUDA(c, cudaMemcpyAsync(d_in1, in1, n * in1_per * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+             "H2D");
+  BLZ_CUDA(c, blz::launch_stage(lc(c), c->basis, stage, d_in0, d_in1, n, d_out0, d_out1, d_out2, d_out3), "stage");
+  auto back = [&](void* h, const void* dv, uint64_t bytes) {
+    return bytes ? cudaMemcpyAsync(h, dv, bytes, cudaMemcpyDeviceToHost, c->stream) : cudaSuccess;
+  };
+  BLZ_CUDA(c, back(out0, d_out0, n * out0_per * sizeof(double)), "D2H");
+  BLZ_CUDA(c, back(out1, d_out1, n * out1_per * sizeof(double)), "D2H");
+  BLZ_CUDA(c, back(out2, d_out2, n * out2_per * sizeof(double)), "D2H");
+  BLZ_CUDA(c, back(out3, d_out3, n * out3_bytes), "D2H");
+  return latch_status(c);
+}
+
+blz_status blz_normalize_blocks(blz_ctx* c, const double* m, uint64_t n, double* first, double* deltas) {
+  return stage_call(c, blz::STAGE_NORMALIZE, m, 64, nullptr, 0, n, deltas, 64, first, 1, nullptr, 0, nullptr, 0);
+}
+blz_status blz_denormalize_blocks(blz_ctx* c, const double* first, const double* deltas, uint64_t n, double* m) {
+  return stage_call(c, blz::STAGE_DENORMALIZE, deltas, 64, first, 1, n, m, 64, nullptr, 0, nullptr, 0, nullptr, 0);
+}
+blz_status blz_mean_slope_blocks(blz_ctx* c, const double* deltas, uint64_t n, double* s) {
+  return stage_call(c, blz::STAGE_MEAN_SLOPE, deltas, 64, nullptr, 0, n, s, 1, nullptr, 0, nullptr, 0, nullptr, 0);
+}
+blz_status blz_predict_blocks(blz_ctx* c, const double* slopes, const double* slope_mean, uint64_t n,
+                              uint8_t* indices, double* snapped, double* lo, double* step) {
+  return stage_call(c, blz::STAGE_PREDICT, slopes, 64, slope_mean, 1, n, snapped, 64, lo, 1, step, 1, indices, 64);
+}
+blz_status blz_quantize_coeffs_blocks(blz_ctx* c, const double* d, uint64_t n, uint8_t* scale, int8_t* coeffs) {
+  // coeffs (n x 28 bytes) travel in the out1 slot, scale bytes in out3
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (n == 0) return BLZ_OK;
+  cudaError_t e;
+  const uint64_t cd = (n * 28 + 7) / 8;
+  double* s = (double*)slot(c, S_IN0, (n * 64 + cd) * sizeof(double) + n + 64, &e);
+  if (!s) return cuda_err(c, e, "scratch allocation");
+  double* d_in = s;
+  double* d_c = d_in + n * 64;
+  uint8_t* d_scale = reinterpret_cast<uint8_t*>(d_c + cd);
+  BLZ_CUDA(c, cudaMemcpyAsync(d_in, d, n * 64 * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+  BLZ_CUDA(c, blz::launch_stage(lc(c), c->basis, blz::STAGE_QUANTIZE, d_in, nullptr, n, nullptr, d_c, nullptr, d_scale),
+           "quantize_coeffs");
+  BLZ_CUDA(c, cudaMemcpyAsync(coeffs, d_c, n * 28, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  BLZ_CUDA(c, cudaMemcpyAsync(scale, d_scale, n, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  return latch_status(c);
+}
+blz_status blz_dct2_blocks(blz_ctx* c, const double* x, uint64_t n, double* d) {
+  return stage_call(c, blz::STAGE_DCT2, x, 64, nullptr, 0, n, d, 64, nullptr, 0, nullptr, 0, nullptr, 0);
+}
+blz_status blz_idct2_blocks(blz_ctx* c, const double* d, uint64_t n, double* x) {
+  return stage_call(c, blz::STAGE_IDCT2, d, 64, nullptr, 0, n, x, 64, nullptr, 0, nullptr, 0, nullptr, 0);
+}
+
 // ---- evaluation harness (H/bench.hpp:67-84) ------------------------------------
 blz_status blz_mean_relative_error_dev(blz_ctx* c, const double* ref, const double* cand, uint64_t n, double* mean,
                                        uint64_t* excluded) {

@@ -61,6 +61,11 @@ cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out);
 cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r);
 cudaError_t launch_sum(const LaunchCtx& c, const double* v, uint64_t n, double* out);
+// stages.cu (batched stage functions of the codec, one thread per block)
+enum StageId { STAGE_NORMALIZE = 1, STAGE_DENORMALIZE, STAGE_MEAN_SLOPE, STAGE_PREDICT, STAGE_QUANTIZE, STAGE_DCT2,
+               STAGE_IDCT2 };
+cudaError_t launch_stage(const LaunchCtx& c, const Basis& B, int stage, const double* in0, const double* in1,
+                         uint64_t n, double* out0, double* out1, double* out2, void* out3);
 // harness.cu (evaluation-harness reduction)
 cudaError_t launch_mean_rel_error(const LaunchCtx& c, const double* ref, const double* cand, uint64_t n,
                                   double* mean, unsigned long long* excluded);

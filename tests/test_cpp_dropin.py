@@ -1,8 +1,8 @@
 """C++ drop-in (include/blaz/blaz.hpp over libblaz_cuda.so) on the GPU.
 
 * tests/cpp/dropin_test: our C++ suite, drop-in vs the C oracle port, bitwise.
-* oracle/_ref/ref_{matrix,block_ops,io,bench}_test_on_dropin: the REFERENCE's
-  own proj/tests/{matrix,block_ops,io,bench}_test.cpp, compiled from
+* oracle/_ref/ref_{matrix,block_ops,codec,dct,io,bench}_test_on_dropin: the
+  REFERENCE's own proj/tests/*_test.cpp (all six files), compiled from
   /root/reference against the drop-in header instead of the reference headers
   (oracle/Makefile target dropin-ref-tests; built where /root/reference
   exists, shipped to the GPU box as binaries).
@@ -22,6 +22,8 @@ BINARIES = [
     os.path.join(ROOT, "oracle", "_ref", "ref_block_ops_test_on_dropin"),
     os.path.join(ROOT, "oracle", "_ref", "ref_io_test_on_dropin"),
     os.path.join(ROOT, "oracle", "_ref", "ref_bench_test_on_dropin"),
+    os.path.join(ROOT, "oracle", "_ref", "ref_codec_test_on_dropin"),
+    os.path.join(ROOT, "oracle", "_ref", "ref_dct_test_on_dropin"),
 ]
 
 
