@@ -374,7 +374,7 @@ def _time(fn, reps, warm=1):
 
 
 def run_extras(args):
-    """Configs 2 and 3 of BASELINE.json on one GPU (reported beside the cfg1 headline)."""
+    """Configs 2, 3 and (one GPU of) 4 of BASELINE.json (reported beside the cfg1 headline)."""
     import numpy as np
     import torch
 
@@ -439,6 +439,37 @@ def run_extras(args):
     out["cfg3"] = rec
     del A, B, C, scratch
     torch.cuda.empty_cache()
+    # ---- config 4 (one GPU of the sharded case): rough-data matmul 32768^3 --------------
+    n4 = args.cfg4_size
+    if n4 > 0:
+        A, a_rows = _chunked_compress("rough", n4, n4, 41)
+        B, _ = _chunked_compress("rough", n4, n4, 42)
+        C = dev.DeviceCMat(n4, n4)
+        scratch = dev.matmul_scratch(A, B)
+        flops = 2.0 * n4 ** 3
+        rec = {"workload": f"cfg4 compressed matmul {n4}^3, rough U[-1,1] data, one GPU (compressed in and out)"}
+        for mode, name in ((1, "fused_dmma"), (0, "exact")):
+            ms = _time(lambda: dev.matmul(A, B, mode=mode, out=C, scratch=scratch), reps=1)
+            tf = flops / (ms * 1e-3) / 1e12
+            rec[name] = {"ms": round(ms, 1), "tflops": round(tf, 2), "frac_fp64_peak": round(tf / fp64_peak, 3)}
+        if not args.no_parity:  # C is the exact-mode result (last run)
+            from oracle import oracle as O
+            if O.ref_available():
+                r = O.ref()
+                ha, hb = A.to_host(), B.to_host()
+                want = r.mat_mul(ha.blocks[:1], 8, n4, hb.blocks, n4, n4, host_threads())
+                hc = C.to_host().blocks[:1]
+                same = all(np.array_equal(np.ascontiguousarray(hc[f]).view(np.uint8),
+                                          np.ascontiguousarray(want[f]).view(np.uint8))
+                           for f in ("first", "slope", "scale_factor", "coeffs"))
+                rec["parity"] = {"sampled_block_rows": 1, "exact_mode_bit_exact": bool(same),
+                                 "against": "the reference (oracle/_ref) mat_mul"}
+                del ha, hb
+        if not args.no_cpu_baseline:
+            rec["cpu_baseline"] = cpu_baseline_matmul(a_rows, n4, gen="rough")
+        out["cfg4_1gpu"] = rec
+        del A, B, C, scratch
+        torch.cuda.empty_cache()
     return out
 
 
@@ -463,7 +494,7 @@ def cpu_baseline_rowdot(a_rows, b_rows, n):
             "sample": f"64 x {n} slice: reference decompress_matrix of A and B + row sums"}
 
 
-def cpu_baseline_matmul(a_rows, n):
+def cpu_baseline_matmul(a_rows, n, gen="smooth"):
     """Reference mat_mul of an 8-row slice of A by the full B (all host threads)."""
     from oracle import oracle as O
     if not O.ref_available():
@@ -471,7 +502,7 @@ def cpu_baseline_matmul(a_rows, n):
     import paper_2202_13007_b200.workloads as W
     r = O.ref()
     threads = host_threads()
-    b = W.smooth_field(n, n, 22).numpy()
+    b = W.smooth_field(n, n, 22).numpy() if gen == "smooth" else W.rough_uniform(n, n, 42).numpy()
     ca = r.compress_matrix(a_rows[:8], threads)
     cb = r.compress_matrix(b, threads)
     t0 = time.perf_counter()
@@ -609,6 +640,7 @@ def main():
     ap.add_argument("--cfg2-size", type=int, default=65536)
     ap.add_argument("--cfg3-size", type=int, default=8192)
     ap.add_argument("--extra-reps", type=int, default=3)
+    ap.add_argument("--cfg4-size", type=int, default=32768, help="0 skips the config-4 one-GPU matmul")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps
     cfg = CONFIGS[args.config]
