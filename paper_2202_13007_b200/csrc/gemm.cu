@@ -20,10 +20,11 @@
 namespace blz {
 
 // ---------------------------------------------------------------------------
-// exact SIMT DGEMM: 128x128 CTA tile, BK = 8, 256 threads, 8x8 per thread
+// exact SIMT DGEMM: 128x128 CTA tile, BK = 16, 256 threads, 8x8 per thread;
+// both operands staged with cp.async (double buffer), one barrier per 16 k.
 // ---------------------------------------------------------------------------
-constexpr int EBM = 128, EBN = 128, EBK = 8;
-constexpr int EAS = EBK + 1;  // A tile row stride (padded): As[m][k]
+constexpr int EBM = 128, EBN = 128, EBK = 16;
+constexpr int EAS = EBK;  // As[m][k] row stride; a warp reads 2 rows per k (broadcast)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   __pipeline_memcpy_async(smem, gmem, 16);
@@ -33,8 +34,9 @@ __global__ void __launch_bounds__(256) k_gemm_exact(const double* __restrict__ A
                                                     const double* __restrict__ Bm, uint64_t ldb,
                                                     double* __restrict__ Cm, uint64_t ldc, uint64_t M,
                                                     uint64_t N, uint64_t K) {
-  __shared__ __align__(16) double As[2][EBM * EAS];
-  __shared__ __align__(16) double Bs[2][EBK * EBN];
+  extern __shared__ __align__(16) double esm[];
+  double* As0 = esm;                      // [2][EBM * EAS]
+  double* Bs0 = esm + 2 * EBM * EAS;      // [2][EBK * EBN]
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const uint64_t m0 = (uint64_t)blockIdx.y * EBM, n0 = (uint64_t)blockIdx.x * EBN;
@@ -42,29 +44,29 @@ __global__ void __launch_bounds__(256) k_gemm_exact(const double* __restrict__ A
   const bool vecB = ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(Bm) & 15) == 0);
 
   auto load_tile = [&](int buf, uint64_t k0) {
-    // A: 128 rows x 8 k = 512 double2 chunks -> 2 per thread
+    double* As = As0 + buf * EBM * EAS;
+    double* Bs = Bs0 + buf * EBK * EBN;
+    // A: 128 rows x 16 k = 1024 double2 chunks -> 4 per thread
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < 4; ++r) {
       const int e = tid + r * 256;
-      const int row = e >> 2, kc = (e & 3) * 2;
+      const int row = e >> 3, kc = (e & 7) * 2;
       const uint64_t gr = m0 + row, gk = k0 + kc;
-      double* dst = &As[buf][row * EAS + kc];
+      double* dst = &As[row * EAS + kc];
       if (gr < M && gk + 1 < K && vecA) {
-        const double2 v = *reinterpret_cast<const double2*>(A + gr * lda + gk);  // 8-byte aligned rows (EAS odd)
-        dst[0] = v.x;
-        dst[1] = v.y;
+        cp_async16(dst, A + gr * lda + gk);
       } else {
         dst[0] = (gr < M && gk < K) ? A[gr * lda + gk] : 0.0;
         dst[1] = (gr < M && gk + 1 < K) ? A[gr * lda + gk + 1] : 0.0;
       }
     }
-    // B: 8 rows x 128 cols = 512 double2 chunks -> 2 per thread (cp.async)
+    // B: 16 rows x 128 cols = 1024 double2 chunks -> 4 per thread
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < 4; ++r) {
       const int e = tid + r * 256;
       const int kr = e >> 6, cc = (e & 63) * 2;
       const uint64_t gk = k0 + kr, gc = n0 + cc;
-      double* dst = &Bs[buf][kr * EBN + cc];
+      double* dst = &Bs[kr * EBN + cc];
       if (gk < K && gc + 1 < N && vecB) {
         cp_async16(dst, Bm + gk * ldb + gc);
       } else {
@@ -92,22 +94,31 @@ __global__ void __launch_bounds__(256) k_gemm_exact(const double* __restrict__ A
       __pipeline_wait_prior(0);
     }
     __syncthreads();
+    const double* As = As0 + buf * EBM * EAS;
+    const double* Bs = Bs0 + buf * EBK * EBN;
 #pragma unroll
-    for (int kk = 0; kk < EBK; ++kk) {
-      double av[8], bv[8];
+    for (int kk = 0; kk < EBK; kk += 2) {
+      // two k steps per smem round: A as (k, k+1) pairs, B rows k and k+1
+      double2 av[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) av[i] = As[buf][(ty * 8 + i) * EAS + kk];
-      // thread columns: (j/2)*32 + 2*tx + (j%2) -- 8 lanes read 128 contiguous bytes
+      for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const double2*>(&As[(ty * 8 + i) * EAS + kk]);
 #pragma unroll
-      for (int j = 0; j < 8; j += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(&Bs[buf][kk * EBN + (j / 2) * 32 + 2 * tx]);
-        bv[j] = v.x;
-        bv[j + 1] = v.y;
+      for (int h = 0; h < 2; ++h) {
+        double bv[8];
+        // thread columns: (j/2)*32 + 2*tx + (j%2) -- 8 lanes read 128 contiguous bytes
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(&Bs[(kk + h) * EBN + (j / 2) * 32 + 2 * tx]);
+          bv[j] = v.x;
+          bv[j + 1] = v.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double a = h ? av[i].y : av[i].x;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = acc[i][j] + a * bv[j];
+        }
       }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = acc[i][j] + av[i] * bv[j];
     }
     __syncthreads();
   }
@@ -243,7 +254,13 @@ cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t 
     k_gemm_dmma<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
   } else {
     dim3 grid((unsigned)((N + EBN - 1) / EBN), (unsigned)((M + EBM - 1) / EBM));
-    k_gemm_exact<<<grid, 256, 0, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
+    const size_t smem = (size_t)(2 * EBM * EAS + 2 * EBK * EBN) * sizeof(double);
+    static bool attr_e = false;
+    if (!attr_e) {
+      cudaFuncSetAttribute(k_gemm_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_e = true;
+    }
+    k_gemm_exact<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
   }
   ++*c.launches;
   return cudaGetLastError();
