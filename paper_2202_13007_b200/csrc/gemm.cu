@@ -136,9 +136,12 @@ __global__ void __launch_bounds__(256) k_gemm_exact(const double* __restrict__ A
 
 // ---------------------------------------------------------------------------
 // fused DGEMM on FP64 tensor cores (DMMA m8n8k4), ascending k
-// CTA tile 128x128, BK = 16, 8 warps (each 64 x 32: 8 x 4 MMA tiles)
+// CTA tile 128x128, BK = 32, 8 warps (each 64 x 32: 8 x 4 MMA tiles)
 // ---------------------------------------------------------------------------
-constexpr int DBM = 128, DBN = 128, DBK = 16;
+#ifndef DMMA_BK
+#define DMMA_BK 32
+#endif
+constexpr int DBM = 128, DBN = 128, DBK = DMMA_BK;
 constexpr int DAS = DBK + 4;   // As[m][k] row stride = 4 mod 16 doubles: conflict-free fragment loads
 constexpr int DBS = DBN + 4;   // Bs[k][n] row stride = 4 mod 16 doubles
 
@@ -158,11 +161,11 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
   auto load_tile = [&](int buf, uint64_t k0) {
     double* As = As0 + buf * DBM * DAS;
     double* Bs = Bs0 + buf * DBK * DBS;
-    // A: 128 x 16 = 1024 16-byte chunks -> 4 per thread
+    // A: 128 x DBK doubles in 16-byte chunks (DBK/2 per row)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < DBK / 4; ++r) {
       const int e = tid + r * 256;
-      const int row = e >> 3, kc = (e & 7) * 2;
+      const int row = e / (DBK / 2), kc = (e % (DBK / 2)) * 2;
       const uint64_t gr = m0 + row, gk = k0 + kc;
       double* dst = As + row * DAS + kc;
       if (vecA && gr < M && gk + 1 < K) {
@@ -172,9 +175,9 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
         dst[1] = (gr < M && gk + 1 < K) ? A[gr * lda + gk + 1] : 0.0;
       }
     }
-    // B: 16 x 128 = 1024 16-byte chunks -> 4 per thread
+    // B: DBK x 128 doubles = DBK * 64 16-byte chunks
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < DBK / 4; ++r) {
       const int e = tid + r * 256;
       const int kr = e >> 6, cc = (e & 63) * 2;
       const uint64_t gk = k0 + kr, gc = n0 + cc;
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                        : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
                        : "d"(fa[i]), "d"(fb[j]));
     }
