@@ -53,16 +53,17 @@ for r in rows[2:]:
         "dram_pct": val(r, "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed") or val(r, "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
         "issue_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "fp64_pct": val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+        "dmma_pct": val(r, "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active"),
         "alu_pct": val(r, "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
         "warps_pct": val(r, "sm__warps_active.avg.pct_of_peak_sustained_active"),
         "regs": int(val(r, "launch__registers_per_thread")),
         "stalls": ", ".join(f"{k}={v:.2f}" for k, v in st[:4]),
     }
-lines = ["| kernel | us | DRAM rd MB | DRAM wr MB | DRAM GB/s | issue % | FP64 % | ALU % | warps % | regs | top stalls |",
-         "|---|---|---|---|---|---|---|---|---|---|---|"]
+lines = ["| kernel | us | DRAM rd MB | DRAM wr MB | DRAM GB/s | issue % | FP64 % | DMMA % | ALU % | warps % | regs | top stalls |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|"]
 for k, v in seen.items():
     lines.append(f"| {k} | {v['us']:.1f} | {v['read_MB']:.1f} | {v['write_MB']:.1f} | {1000.0 * (v['read_MB'] + v['write_MB']) / max(v['us'], 1e-9):.0f} | "
-                 f"{v['issue_pct']:.1f} | {v['fp64_pct']:.1f} | {v['alu_pct']:.1f} | {v['warps_pct']:.1f} | "
+                 f"{v['issue_pct']:.1f} | {v['fp64_pct']:.1f} | {v['dmma_pct']:.1f} | {v['alu_pct']:.1f} | {v['warps_pct']:.1f} | "
                  f"{v['regs']} | {v['stalls']} |")
 out = "\n".join(lines)
 print(out)
