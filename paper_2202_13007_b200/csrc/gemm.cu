@@ -249,20 +249,16 @@ cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t 
   if (mode == 1) {
     dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
     const size_t smem = (size_t)(2 * DBM * DAS + 2 * DBK * DBS) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    // per call: the attribute belongs to the current device (a few microseconds
+    // against a GEMM of milliseconds)
+    cudaError_t ea = cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return ea;
     k_gemm_dmma<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
   } else {
     dim3 grid((unsigned)((N + EBN - 1) / EBN), (unsigned)((M + EBM - 1) / EBM));
     const size_t smem = (size_t)(2 * EBM * EAS + 2 * EBK * EBN) * sizeof(double);
-    static bool attr_e = false;
-    if (!attr_e) {
-      cudaFuncSetAttribute(k_gemm_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr_e = true;
-    }
+    cudaError_t ea = cudaFuncSetAttribute(k_gemm_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return ea;
     k_gemm_exact<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
   }
   ++*c.launches;
