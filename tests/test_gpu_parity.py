@@ -430,3 +430,49 @@ def test_mean_relative_error_serial_order():
     with pytest.raises(blz.InvalidArgument, match="dimension mismatch"):
         ctx.check(ctx.lib.blz_mean_relative_error(ctx.handle, a.ctypes.data, 50, 100, b.ctypes.data, 100, 50,
                                                   C.byref(mean), C.byref(exc)))
+
+
+def _equal_cmats(x, y):
+    return all(torch.equal(getattr(x, f), getattr(y, f)) for f in ("first", "slope", "scale", "coeffs"))
+
+
+@pytest.mark.parametrize("gen", ["quadratic", "rough"])
+def test_full_size_properties(gen):
+    """BASELINE config-1 size (16384^2, 4.19 M blocks): size-independent properties.
+
+    * the verified fast compress equals the reference-order exact kernel on EVERY block;
+    * the shared-product decompress equals the plain reference-order kernel bitwise;
+    * add commutes bitwise; scale by 1 and by 2 then 0.5 are identities; A - A is zero;
+    * the fused chains equal the two-call chains.
+    """
+    n = 16384
+    a = W.make(gen, n, n, seed=71, device="cuda")
+    b = W.make(gen, n, n, seed=72, device="cuda")
+    dctx = dev.context()
+    ca, cb = dev.compress(a), dev.compress(b)
+    dctx.set_mode(blz.MODE_EXACT)
+    try:
+        ea = dev.compress(a)
+        exact_dense = dev.decompress(ca)
+        dev.sync()
+    finally:
+        dctx.set_mode(blz.MODE_DEFAULT)
+    assert _equal_cmats(ca, ea)
+    del a, b, ea
+    fast_dense = dev.decompress(ca)
+    dev.sync()
+    assert torch.equal(fast_dense.view(torch.int64), exact_dense.view(torch.int64))
+    del exact_dense
+    assert _equal_cmats(dev.add(ca, cb), dev.add(cb, ca))
+    assert _equal_cmats(dev.scale(ca, 1.0), ca)
+    assert _equal_cmats(dev.scale(dev.scale(ca, 2.0), 0.5), ca)
+    zero = dev.decompress(dev.sub(ca, ca))
+    dev.sync()
+    assert not bool(zero.any())
+    del zero
+    out, dense = dev.sub_decompress(ca, cb, dense=fast_dense)
+    ref_c = dev.sub(ca, cb)
+    ref_d = dev.decompress(ref_c)
+    dev.sync()
+    assert _equal_cmats(out, ref_c)
+    assert torch.equal(dense.view(torch.int64), ref_d.view(torch.int64))
