@@ -22,7 +22,13 @@
 
 namespace blz {
 
-constexpr int PAIR_WARPS = 4;  // 128-thread CTA = 2 warp pairs
+#ifndef CP_PAIR_WARPS
+#define CP_PAIR_WARPS 2
+#endif
+#ifndef CP_MINB
+#define CP_MINB 8
+#endif
+constexpr int PAIR_WARPS = CP_PAIR_WARPS;  // 64-thread CTA = one warp pair (8 CTAs / SM)
 
 // Butterfly constants (exact-math DCT-II, correctly rounded on the host):
 // c[0] = 1/sqrt(8), c[k] = cos(k pi/16)/2.  half[h] holds the pass-1
@@ -101,7 +107,7 @@ __device__ __forceinline__ void dct8_f64(const double (&c)[8], const double (&z)
   y[7] = fma(c[7], d0, fma(-c[5], d1, fma(c[3], d2, -(c[1] * d3))));
 }
 
-__global__ void __launch_bounds__(PAIR_WARPS * 32, 4)
+__global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     k_compress_pair(const FastParams P, const Butterfly W, const double* __restrict__ dense, uint64_t rows,
                     uint64_t cols, uint64_t ld, CMat out, uint64_t* __restrict__ wl,
                     unsigned long long* __restrict__ wl_count) {
