@@ -599,7 +599,7 @@ blz_status ensure_pipe(blz_ctx* c, size_t nev) {
 }
 
 template <class H2D, class Compute, class D2H>
-blz_status pipelined(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compute, D2H&& d2h) {
+blz_status pipelined_body(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compute, D2H&& d2h) {
   uint64_t step = (block_rows + 15) / 16;
   step = (step + 15) / 16 * 16;
   if (step < 16) step = 16;
@@ -619,9 +619,21 @@ blz_status pipelined(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compu
     BLZ_CUDA(c, cudaStreamWaitEvent(c->s_out, k_done, 0), "event");
     BLZ_CUDA(c, d2h(b0, b1, c->s_out), "D2H");
   }
-  BLZ_CUDA(c, cudaStreamSynchronize(c->s_out), "sync");
-  BLZ_CUDA(c, cudaStreamSynchronize(c->s_in), "sync");
   return BLZ_OK;
+}
+
+// Runs the chunk pipeline and always drains all three streams before returning,
+// so no copy touches the caller's host buffers after the call (also on errors).
+template <class H2D, class Compute, class D2H>
+blz_status pipelined(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compute, D2H&& d2h) {
+  const blz_status st = pipelined_body(c, block_rows, h2d, compute, d2h);
+  const cudaError_t e1 = c->s_out ? cudaStreamSynchronize(c->s_out) : cudaSuccess;
+  const cudaError_t e2 = c->s_in ? cudaStreamSynchronize(c->s_in) : cudaSuccess;
+  const cudaError_t e3 = cudaStreamSynchronize(c->stream);
+  if (st != BLZ_OK) return st;
+  if (e1 != cudaSuccess) return cuda_err(c, e1, "sync");
+  if (e2 != cudaSuccess) return cuda_err(c, e2, "sync");
+  return cuda_err(c, e3, "sync");
 }
 
 // device AoS staging for block-row range [b0, b1) of a (rows x cols) grid
