@@ -36,7 +36,15 @@ def local_rows(rows: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def gather_uneven(t: torch.Tensor, group=None) -> torch.Tensor:
-    """All-gather along dim 0 with per-rank sizes that may differ; rank order."""
+    """All-gather along dim 0 with per-rank sizes that may differ; rank order.
+
+    NCCL gathers device tensors directly; other backends (gloo: CPU tests, the
+    single-GPU multi-rank dry run) go through host memory.  Without a process
+    group (one process) the local tensor is the whole result."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return t
+    if t.is_cuda and dist.get_backend(group) != "nccl":
+        return gather_uneven(t.cpu(), group).to(t.device)
     world = dist.get_world_size(group)
     n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
@@ -80,6 +88,12 @@ def frobenius_allreduce(a_local, b_local, group=None):
     """Per-rank ascending partial totals, summed by one allreduce (tolerance parity)."""
     from . import device as dev
     part = dev.sum_ascending(dev.rowdot(a_local, b_local))
+    if not (dist.is_available() and dist.is_initialized()):
+        return part
+    if part.is_cuda and dist.get_backend(group) != "nccl":
+        host = part.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        return host.to(part.device)
     dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
     return part
 
