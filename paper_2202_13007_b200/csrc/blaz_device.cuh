@@ -76,6 +76,18 @@ __device__ __forceinline__ bool is_finite(double v) {
 __device__ __forceinline__ void put_coeff(uint32_t (&w)[7], int k, int c) {
   w[k >> 2] |= (uint32_t)(c & 0xff) << (8 * (k & 3));
 }
+// Byte q of w as a signed int8, converted to double: one I2F.F64.S8 with a byte
+// selector (byte 0 through PTX cvt.s8, which C++ sign extension would turn into
+// two PRMTs and an I2F.S16).
+__device__ __forceinline__ double i8_byte_to_f64(uint32_t w, int q) {
+  if (q == 0) {
+    double d;
+    asm("cvt.rn.f64.s8 %0, %1;" : "=d"(d) : "h"((unsigned short)w));
+    return d;
+  }
+  return (double)(int8_t)(uint8_t)(w >> (8 * q));
+}
+
 __device__ __forceinline__ int get_coeff(const uint32_t (&w)[7], int k) {
   return (int)(int8_t)(uint8_t)(w[k >> 2] >> (8 * (k & 3)));
 }

@@ -76,8 +76,8 @@ __device__ __forceinline__ CombineOut combine_record(double f1, double s1, uint3
       int n[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double x1 = (double)(int8_t)(uint8_t)(c1[w] >> (8 * q));  // I2F.F64.S8 on a byte lane
-        const double x2 = (double)(int8_t)(uint8_t)(c2[w] >> (8 * q));
+        const double x1 = i8_byte_to_f64(c1[w], q);  // I2F.F64.S8 on a byte lane
+        const double x2 = i8_byte_to_f64(c2[w], q);
         n[q] = round_clamp_coeff(o.w1 * x1 + o.w2 * x2);  // (:55-56)
       }
       o.c[w] = __byte_perm(__byte_perm(n[0], n[1], 0x0040), __byte_perm(n[2], n[3], 0x0040), 0x5410);
