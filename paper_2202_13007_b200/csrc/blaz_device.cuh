@@ -202,6 +202,11 @@ __device__ __forceinline__ uint32_t compress_exact(double (&m)[BC], const Basis&
 // r = RN(1/phi), q = RN(C*r), e = C - phi*q (exact in one FMA), RN(q + e*r).
 // Equal to the IEEE quotient over the whole 256 x 255 domain (checked
 // exhaustively, tests/test_oracle_golden.py::test_markstein_dequant_exhaustive).
+__device__ __forceinline__ double dequant_d(double cd, double phi, double r) {
+  const double q = cd * r;
+  const double e = fma(-phi, q, cd);
+  return fma(e, r, q);
+}
 __device__ __forceinline__ double dequant(int c, double phi, double r) {
   const double cd = (double)c;
   const double q = cd * r;
@@ -225,7 +230,7 @@ __device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basi
   if (b.phi - 1u < 255u) {
     const double r = 1.0 / fphi;
 #pragma unroll
-    for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : dequant(get_coeff(b.c, k), fphi, r);
+    for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : dequant_d(i8_byte_to_f64(b.c[k >> 2], k & 3), fphi, r);
   } else {
 #pragma unroll
     for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : (double)get_coeff(b.c, k) / fphi;
