@@ -74,7 +74,7 @@ __device__ __forceinline__ uint32_t decide_byte(double y, uint32_t mq, uint32_t&
   const int hi = (int)hi32(t);
   const int c = min(max(hi, 0x41380000 + LO), 0x41380000 + HI);
   kmin = min(kmin, lo32(t) + mq);
-  return (uint32_t)c & 0xffu;
+  return (uint32_t)c;  // callers take the low byte
 }
 
 // Outputs 4h..4h+3 of the 8-point transform of the integer vector k[0..7]:
@@ -248,10 +248,11 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     // ---- quantizer indices for the 32 own cells ---------------------------
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-      uint32_t word = 0;
+      uint32_t c[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) word |= decide_byte<0, 255>(fma(m[w * 4 + q], A, Bc), mq_x, kmin) << (8 * q);
-      sh.idx[lane][h * 8 + w] = word;
+      for (int q = 0; q < 4; ++q) c[q] = decide_byte<0, 255>(fma(m[w * 4 + q], A, Bc), mq_x, kmin);
+      // low byte of each decision into one word (three byte permutes)
+      sh.idx[lane][h * 8 + w] = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
     }
     bool near = kmin < 2u * mq_x;
     pair_bar(bar);    // B3: full index grid visible
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
       for (int c = 0; c < 2; ++c) {
         const double gv = ii < 2 ? G[ii * 8 + c] : G[16 + (ii - 2) * 2 + c];
         const double y = (h == 0 && ii == 0 && c == 0) ? phi * d00 : gv * ps;
-        const uint32_t byte = decide_byte<-127, 127>(y, mq_c, kmin);
+        const uint32_t byte = decide_byte<-127, 127>(y, mq_c, kmin) & 0xffu;
         const int r = 4 * h + ii;
         const int k = r < 2 ? 8 * r + c : (c == 0 ? 14 + r : 20 + r);
         cb[k] = zero_c ? 0 : (uint8_t)byte;
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
       for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
         for (int c = 2; c < 8; ++c) {
-          const uint32_t byte = decide_byte<-127, 127>(G[ii * 8 + c] * ps, mq_c, kmin);
+          const uint32_t byte = decide_byte<-127, 127>(G[ii * 8 + c] * ps, mq_c, kmin) & 0xffu;
           cb[8 * ii + c] = zero_c ? 0 : (uint8_t)byte;
         }
     }
