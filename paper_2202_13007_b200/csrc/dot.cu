@@ -57,6 +57,65 @@ __global__ void __launch_bounds__(128) k_dot_entries(const Basis B, CMat a, CMat
   }
 }
 
+// Few queries: one warp per query.  Lanes decompress the pairs (A(bi, t), B(t, bj))
+// for 32 consecutive t at once and form the products a(ri, k) * b(k, cj) (each
+// rounded, as the reference's r += a * b); lane 0 then adds them in the
+// reference's order (t ascending, then k < klim) -- the same operation sequence
+// as the thread-per-query kernel, with the decompressions spread over the warp.
+template <bool SYM>
+__global__ void __launch_bounds__(128) k_dot_warp(const Basis B, CMat a, CMat b, const uint64_t* __restrict__ qi,
+                                                 const uint64_t* __restrict__ qj, uint64_t n,
+                                                 double* __restrict__ out, unsigned long long* err) {
+  __shared__ double prod[4][32 * 9];  // per warp: 8 products per lane (+1 pad)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* pw = prod[warp];
+  for (uint64_t q = blockIdx.x * (uint64_t)4 + warp; q < n; q += (uint64_t)gridDim.x * 4) {
+    const uint64_t i = qi[q], j = qj[q];
+    if (i >= a.rows || j >= b.cols) {  // warp-uniform
+      if (lane == 0) {
+        latch_error(err, q, DERR_DOT_RANGE);
+        out[q] = 0.0;
+      }
+      continue;
+    }
+    const uint64_t bi = i / BD, bj = j / BD;
+    const int ri = (int)(i % BD), cj = (int)(j % BD);
+    double r = 0.0;
+    for (uint64_t t0 = 0; t0 < a.bc; t0 += 32) {
+      const uint64_t t = min(t0 + lane, a.bc - 1);
+      double arow[BD], bcol[BD];
+      const RBlock ba = load_block(a, bi * a.bc + t);
+      const RBlock bb = load_block(b, t * b.bc + bj);
+      decompress_exact<SYM>(ba, B, [&](int u, const double (&row)[BD]) {
+        if (u == ri) {
+#pragma unroll
+          for (int k = 0; k < BD; ++k) arow[k] = row[k];
+        }
+      });
+      decompress_exact<SYM>(bb, B, [&](int u, const double (&row)[BD]) {
+        double v = row[0];
+#pragma unroll
+        for (int k = 1; k < BD; ++k) v = (cj == k) ? row[k] : v;
+        bcol[u] = v;
+      });
+#pragma unroll
+      for (int k = 0; k < BD; ++k) pw[lane * 9 + k] = arow[k] * bcol[k];
+      __syncwarp();
+      if (lane == 0) {
+        const uint64_t left = a.bc - t0;
+        const uint64_t cnt = left < 32 ? left : 32;
+        for (uint64_t tl = 0; tl < cnt; ++tl) {
+          const uint64_t rem = a.cols - (t0 + tl) * BD;
+          const int klim = rem < BD ? (int)rem : BD;
+          for (int k = 0; k < klim; ++k) r += pw[tl * 9 + k];
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) out[q] = r;
+  }
+}
+
 // Row dots r_i = sum_j Ahat(i,j) Bhat(i,j), ascending j from +0.0.
 // A warp covers 4 block-rows.  Per chunk of 4 block-columns, lanes 0-15
 // decompress the 16 A blocks and lanes 16-31 the 16 matching B blocks (exact,
@@ -137,6 +196,16 @@ __global__ void k_sum(const double* __restrict__ v, uint64_t n, double* __restri
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out) {
   if (n == 0) return cudaSuccess;
+  const bool sym = c.basis_sym && !c.exact_only;
+  if (n <= (uint64_t)c.sm_count * 64) {  // few queries: a warp per query
+    const unsigned gw = (unsigned)((n + 3) / 4);
+    if (sym)
+      k_dot_warp<true><<<gw, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
+    else
+      k_dot_warp<false><<<gw, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
+    ++*c.launches;
+    return cudaGetLastError();
+  }
   const unsigned g = (unsigned)((n + 127) / 128 < (uint64_t)c.sm_count * 16 ? (n + 127) / 128
                                                                              : (uint64_t)c.sm_count * 16);
   if (c.basis_sym && !c.exact_only)
