@@ -159,6 +159,28 @@ blz_status blz_matmul_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, in
                           void* scratch, const blz_cmat* out);
 blz_status blz_matmul_dense_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, int mode,
                                 void* scratch, double* out, uint64_t ld);
+/* ---- block-row sharded operations over NCCL --------
+ * `nccl_comm` is an ncclComm_t of G ranks (one GPU each); rank r owns
+ * block-rows [BR*r/G, BR*(r+1)/G) of every operand and result.  NCCL is
+ * loaded at run time (libnccl.so.2); without it these return
+ * BLZ_NOT_SUPPORTED.  Stream-ordered on the context stream.
+ *   allgather_cmat: the whole compressed matrix `full` from the row shards
+ *     (45 B per block over NVLink instead of 512 B of binary64);
+ *   rowdot_frobenius: config 2 -- local row dots, all r_i gathered in row order
+ *     into r_all (rows_total entries) and their ascending total (bit-identical
+ *     to the one-GPU result for every G);
+ *   frobenius_allreduce: per-rank ascending partials summed by one allreduce
+ *     (tolerance parity); r_local has a_local->rows entries;
+ *   matmul: config 4 -- gathers B into b_full, then C rows = A rows x B
+ *     (H/matrix.hpp:223-235); scratch: blz_matmul_scratch_bytes(a_local, b_full). */
+blz_status blz_allgather_cmat_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* local, const blz_cmat* full);
+blz_status blz_rowdot_frobenius_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local,
+                                     const blz_cmat* b_local, uint64_t rows_total, double* r_all, double* total);
+blz_status blz_frobenius_allreduce_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local,
+                                        const blz_cmat* b_local, double* r_local, double* total);
+blz_status blz_matmul_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local, const blz_cmat* b_local,
+                           const blz_cmat* b_full, int mode, void* scratch, const blz_cmat* c_local);
+
 /* AoS (48-byte blz_block, device memory) <-> SoA conversions. */
 blz_status blz_pack_aos_dev(blz_ctx* ctx, const blz_cmat* in, blz_block* out);
 blz_status blz_unpack_aos_dev(blz_ctx* ctx, const blz_block* in, const blz_cmat* out);

@@ -81,6 +81,11 @@ SIGNATURES = {
     "blz_add_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_sub_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_scale_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
+    "blz_allgather_cmat_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
+    "blz_rowdot_frobenius_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _U64, _P, _P]),
+    "blz_frobenius_allreduce_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _P]),
+    "blz_matmul_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.c_int, _P,
+                               C.POINTER(blz_cmat)]),
     "blz_normalize_blocks": (_ST, [_P, _P, _U64, _P, _P]),
     "blz_denormalize_blocks": (_ST, [_P, _P, _P, _U64, _P]),
     "blz_mean_slope_blocks": (_ST, [_P, _P, _U64, _P]),

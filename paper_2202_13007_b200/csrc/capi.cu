@@ -299,6 +299,11 @@ void* blz_ctx_get_stream(const blz_ctx* c) { return c ? (void*)c->stream : nullp
 
 const char* blz_last_error(const blz_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+// for the other translation units of the library (sharded.cu); not exported
+__attribute__((visibility("hidden"))) blz_status blz_internal_set_error(blz_ctx* c, blz_status st, const char* msg) {
+  return set_err(c, st, msg);
+}
+
 blz_status blz_ctx_sync(blz_ctx* c) {
   if (!c) return BLZ_INVALID_ARGUMENT;
   return latch_status(c);

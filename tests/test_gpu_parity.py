@@ -476,3 +476,53 @@ def test_full_size_properties(gen):
     dev.sync()
     assert _equal_cmats(out, ref_c)
     assert torch.equal(dense.view(torch.int64), ref_d.view(torch.int64))
+
+
+def _nccl_comm_single_gpu():
+    """A one-rank NCCL communicator on cuda:0 (ncclCommInitAll via ctypes)."""
+    import ctypes as C
+    try:
+        lib = C.CDLL("libnccl.so.2", mode=C.RTLD_GLOBAL)
+    except OSError:
+        pytest.skip("libnccl.so.2 not loadable")
+    comm = C.c_void_p()
+    devs = (C.c_int * 1)(0)
+    assert lib.ncclCommInitAll(C.byref(comm), 1, devs) == 0
+    return lib, comm
+
+
+def test_nccl_sharded_entry_points_one_rank():
+    """The NCCL C-ABI variants with G = 1 equal the local operations bitwise
+    (rank/row-range logic is shared with shard.py, covered by the gloo tests)."""
+    import ctypes as C
+    lib_nccl, comm = _nccl_comm_single_gpu()
+    ctx = dev.context()
+    lib = ctx.lib
+    n = 1000
+    a = dev.compress(torch.from_numpy(W.smooth_field(n, 776, seed=5).numpy()).cuda())
+    b = dev.compress(torch.from_numpy(W.smooth_field(n, 776, seed=6).numpy()).cuda())
+    # config 2: gathered row dots + ascending total
+    r_all = torch.empty(n, dtype=torch.float64, device="cuda")
+    tot = torch.empty(1, dtype=torch.float64, device="cuda")
+    ctx.check(lib.blz_rowdot_frobenius_nccl(ctx.handle, comm, a.ref(), b.ref(), n, C.c_void_p(r_all.data_ptr()),
+                                            C.c_void_p(tot.data_ptr())))
+    r_ref, t_ref = dev.frobenius(a, b)
+    dev.sync()
+    assert torch.equal(r_all.view(torch.int64), r_ref.view(torch.int64))
+    assert torch.equal(tot.view(torch.int64), t_ref.view(torch.int64))
+    # allgather of a compressed matrix (one shard = the whole matrix)
+    full = dev.DeviceCMat(n, 776)
+    ctx.check(lib.blz_allgather_cmat_nccl(ctx.handle, comm, a.ref(), full.ref()))
+    dev.sync()
+    assert all(torch.equal(getattr(full, f), getattr(a, f)) for f in ("first", "slope", "coeffs", "scale"))
+    # config 4: matmul with the gathered B (B^T-shaped second operand)
+    bt = dev.compress(torch.from_numpy(W.smooth_field(776, n, seed=7).numpy()).cuda())
+    b_full = dev.DeviceCMat(776, n)
+    scratch = dev.matmul_scratch(a, b_full)
+    c_sh = dev.DeviceCMat(n, n)
+    ctx.check(lib.blz_matmul_nccl(ctx.handle, comm, a.ref(), bt.ref(), b_full.ref(), 0,
+                                  C.c_void_p(scratch.data_ptr()), c_sh.ref()))
+    c_ref = dev.matmul(a, bt, mode=0)
+    dev.sync()
+    assert all(torch.equal(getattr(c_sh, f), getattr(c_ref, f)) for f in ("first", "slope", "coeffs", "scale"))
+    lib_nccl.ncclCommDestroy(comm)
