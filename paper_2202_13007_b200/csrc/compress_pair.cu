@@ -68,9 +68,15 @@ __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64
 //    so with the certified error m < 1/2 the reference rounds to >= HI (<= LO) and
 //    clamps to the same end.  (Magnitudes stay far below the int64 range where the
 //    reference's conversion misbehaves: see the exponent and m_hi guards.)
+//
+// Callers pass t itself, formed by ONE fused operation: t = fma(g, ps, M) for a
+// coefficient (one rounding to the 2^-32 grid instead of RN(y) then RN(y + M):
+// strictly less error than the margin assumes) and t = fma(delta, A, Bc + M) for
+// a quantizer index (RN(Bc + M) adds at most 2^-33, so that margin carries one
+// more unit of 2^-32).
+constexpr double kDecideM = 1572864.5;  // 1.5 * 2^20 + 0.5
 template <int LO, int HI>
-__device__ __forceinline__ uint32_t decide_byte(double y, uint32_t mq, uint32_t& kmin) {
-  const double t = y + 1572864.5;
+__device__ __forceinline__ uint32_t decide_byte(double t, uint32_t mq, uint32_t& kmin) {
   const int hi = (int)hi32(t);
   const int c = min(max(hi, 0x41380000 + LO), 0x41380000 + HI);
   kmin = min(kmin, lo32(t) + mq);
@@ -241,7 +247,9 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     const double inv_step = 1.0 / step;
     const double A = (1.0 / s) * inv_step;
     const double Bc = -lo * inv_step;
-    const uint32_t mq_x = margin32(2.2737367544323206e-13 * (1.0 + fabs(lo) / smax));
+    const double BcM = Bc + kDecideM;  // rounded: <= 2^-33, the extra unit below
+    uint32_t mq_x = margin32(2.2737367544323206e-13 * (1.0 + fabs(lo) / smax));
+    mq_x += mq_x < 0x7FFFFFFFu ? 1u : 0u;
     if (mq_x >= 0x7FFFFFFFu) status = (status == DERR_NONE) ? NEED_EXACT : status;
     uint32_t kmin = 0xFFFFFFFFu;  // min over decisions of (frac + m) mod 2^32
 
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     for (int w = 0; w < 8; ++w) {
       uint32_t c[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] = decide_byte<0, 255>(fma(m[w * 4 + q], A, Bc), mq_x, kmin);
+      for (int q = 0; q < 4; ++q) c[q] = decide_byte<0, 255>(fma(m[w * 4 + q], A, BcM), mq_x, kmin);
       // low byte of each decision into one word (three byte permutes)
       sh.idx[lane][h * 8 + w] = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
     }
@@ -322,8 +330,8 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const double gv = ii < 2 ? G[ii * 8 + c] : G[16 + (ii - 2) * 2 + c];
-        const double y = (h == 0 && ii == 0 && c == 0) ? phi * d00 : gv * ps;
-        const uint32_t byte = decide_byte<-127, 127>(y, mq_c, kmin) & 0xffu;
+        const double t = (h == 0 && ii == 0 && c == 0) ? fma(phi, d00, kDecideM) : fma(gv, ps, kDecideM);
+        const uint32_t byte = decide_byte<-127, 127>(t, mq_c, kmin) & 0xffu;
         const int r = 4 * h + ii;
         const int k = r < 2 ? 8 * r + c : (c == 0 ? 14 + r : 20 + r);
         cb[k] = zero_c ? 0 : (uint8_t)byte;
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
       for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
         for (int c = 2; c < 8; ++c) {
-          const uint32_t byte = decide_byte<-127, 127>(G[ii * 8 + c] * ps, mq_c, kmin) & 0xffu;
+          const uint32_t byte = decide_byte<-127, 127>(fma(G[ii * 8 + c], ps, kDecideM), mq_c, kmin) & 0xffu;
           cb[8 * ii + c] = zero_c ? 0 : (uint8_t)byte;
         }
     }
