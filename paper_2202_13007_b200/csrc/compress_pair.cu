@@ -36,7 +36,12 @@ constexpr int PAIR_WARPS = CP_PAIR_WARPS;  // 64-thread CTA = one warp pair (8 C
 struct Butterfly {
   double c[8];
   double half[2][11];
+  double c2[2][8];  // pass-2 constants per half; the lower half's odd ones negated
 };
+
+#ifndef CP_COLSPLIT
+#define CP_COLSPLIT 1
+#endif
 
 struct PairShared {
   double sumA[32];
@@ -48,6 +53,9 @@ struct PairShared {
   double d00[32];
   uint32_t nearL[32];
   uint8_t cbytes[32 * 28];  // staged coefficient records of the 32 blocks
+#if CP_COLSPLIT
+  double2 zx[2][8][32];     // pass-1 outputs for the other half's rows [writer][slot][lane]
+#endif
 };
 
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
@@ -265,6 +273,77 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     bool near = kmin < 2u * mq_x;
     pair_bar(bar);    // B3: full index grid visible
 
+#if CP_COLSPLIT
+    // ---- DCT of the index grid: pass 1 over this half's 4 columns ----------
+    // Columns are taken in the order col(c) = h ? 7 - c : c.  All 8 outputs of a
+    // column share one set of integer butterflies: the own rows' outputs use
+    // half[h], the other half's rows half[1 - h] (the same formulas as
+    // dct8_int_half, so every value is the one the row-split version computed).
+    // own[ii][c] = Z(4h + ii, col(c)); the other rows' outputs go to shared memory.
+    double own[4][4];
+    {
+      double ho[11], hx[11];
+#pragma unroll
+      for (int k = 0; k < 11; ++k) {
+        ho[k] = W.half[h][k];
+        hx[k] = W.half[1 - h][k];
+      }
+      uint32_t wv[8];
+#pragma unroll
+      for (int u = 0; u < BD; ++u) wv[u] = sh.idx[lane][u * 2 + h];
+      double oth[4][4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int sft = 8 * (h ? 3 - c : c);
+        int kk[8];
+#pragma unroll
+        for (int u = 0; u < BD; ++u) kk[u] = (int)((wv[u] >> sft) & 0xffu);
+        double yo[4], yx[4];
+        dct8_int_half(ho, h, kk, yo);
+        dct8_int_half(hx, 1 - h, kk, yx);
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          own[ii][c] = yo[ii];
+          oth[ii][c] = yx[ii];
+        }
+      }
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) sh.zx[h][ii * 2 + q][lane] = make_double2(oth[ii][2 * q], oth[ii][2 * q + 1]);
+    }
+    pair_bar(bar);    // B3b: the other half's pass-1 outputs visible
+    // ---- pass 2 (own rows), max|G| and the retained entries ---------------
+    // Row ii of Z in butterfly form: z[j] + z[7-j] = own[j] + B[j] and
+    // z[j] - z[7-j] = +-(own[j] - B[j]) (sign - for h = 1, folded into c2[1]).
+    uint32_t gh = 0;
+    double G[20];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      double B[4];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double2 x = sh.zx[1 - h][ii * 2 + q][lane];
+        B[2 * q] = x.x;
+        B[2 * q + 1] = x.y;
+      }
+      double z[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        z[j] = own[ii][j];
+        z[7 - j] = B[j];
+      }
+      double gr[8];
+      dct8_f64(W.c2[h], z, gr);
+#pragma unroll
+      for (int j = 0; j < BD; ++j) {
+        const uint32_t a = hi32(gr[j]) & 0x7FFFFFFFu;
+        gh = (ii == 0 && j == 0 && h == 0) ? gh : max(gh, a);
+        if (ii < 2) G[ii * 8 + j] = gr[j];
+        else if (j < 2) G[16 + (ii - 2) * 2 + j] = gr[j];
+      }
+    }
+#else
     // ---- DCT of the index grid: pass 1 (columns, outputs 4h..4h+3) --------
     double hc[11];
 #pragma unroll
@@ -299,6 +378,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
         else if (j < 2) G[16 + (ii - 2) * 2 + j] = gr[j];
       }
     }
+#endif
     sh.gh[h][lane] = gh;
     if (h == 0) sh.d00[lane] = fma(step, G[0], lo * P.ss00);
     pair_bar(bar);    // B4
@@ -383,6 +463,10 @@ cudaError_t launch_compress_pair(const LaunchCtx& c, const FastParams& P, const 
   for (int k = 0; k < 11; ++k) {
     W.half[0][k] = up[k];
     W.half[1][k] = lw[k];
+  }
+  for (int k = 0; k < 8; ++k) {
+    W.c2[0][k] = C[k];
+    W.c2[1][k] = (k & 1) ? -C[k] : C[k];
   }
   const uint64_t groups = (out.nb() + 31) / 32;
   const uint64_t want = (groups + PAIR_WARPS / 2 - 1) / (PAIR_WARPS / 2);
