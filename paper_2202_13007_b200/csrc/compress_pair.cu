@@ -208,18 +208,27 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     // cells is 0 iff some delta is +-0 (delta(0,0) = 0 of the upper half is known).
     // The running maximum is kept as words: one FP64 compare and two 32-bit
     // selects per cell, the high word's sign cleared by the select's |.|.
+    // Two independent chains (even / odd cells), merged at the end: the maximum
+    // is exact in any order, and the split halves the compare-select latency.
     uint32_t zmin = 0xFFFFFFFFu;
-    float amax_h = 0.0f;
-    uint32_t amax_l = 0;
+    float amax_h[2] = {0.0f, 0.0f};
+    uint32_t amax_l[2] = {0u, 0u};
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      const bool gt = fabs(m[k]) > __hiloint2double(__float_as_int(amax_h), (int)amax_l);
-      amax_h = gt ? fabsf(__int_as_float((int)hi32(m[k]))) : amax_h;
-      amax_l = gt ? lo32(m[k]) : amax_l;
+      const int c = k & 1;
+      const bool gt = fabs(m[k]) > __hiloint2double(__float_as_int(amax_h[c]), (int)amax_l[c]);
+      amax_h[c] = gt ? fabsf(__int_as_float((int)hi32(m[k]))) : amax_h[c];
+      amax_l[c] = gt ? lo32(m[k]) : amax_l[c];
       const uint32_t zk = (hi32(m[k]) & 0x7FFFFFFFu) | lo32(m[k]);
       zmin = min(zmin, (k == 0 && h == 0) ? 0xFFFFFFFFu : zk);
     }
-    amax = __hiloint2double(__float_as_int(amax_h), (int)amax_l);
+    {
+      const bool gt = __hiloint2double(__float_as_int(amax_h[1]), (int)amax_l[1]) >
+                      __hiloint2double(__float_as_int(amax_h[0]), (int)amax_l[0]);
+      amax_h[0] = gt ? amax_h[1] : amax_h[0];
+      amax_l[0] = gt ? amax_l[1] : amax_l[0];
+    }
+    amax = __hiloint2double(__float_as_int(amax_h[0]), (int)amax_l[0]);
     int nz = 32 - (h == 0);
     if (zmin == 0) {  // some zero deltas (rare on real data): count them
       nz = 0;
@@ -259,17 +268,19 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     uint32_t mq_x = margin32(2.2737367544323206e-13 * (1.0 + fabs(lo) / smax));
     mq_x += mq_x < 0x7FFFFFFFu ? 1u : 0u;
     if (mq_x >= 0x7FFFFFFFu) status = (status == DERR_NONE) ? NEED_EXACT : status;
-    uint32_t kmin = 0xFFFFFFFFu;  // min over decisions of (frac + m) mod 2^32
+    // min over decisions of (frac + m) mod 2^32, in two chains (odd / even cells)
+    uint32_t kmin = 0xFFFFFFFFu, kmin2 = 0xFFFFFFFFu;
 
     // ---- quantizer indices for the 32 own cells ---------------------------
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
       uint32_t c[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] = decide_byte<0, 255>(fma(m[w * 4 + q], A, BcM), mq_x, kmin);
+      for (int q = 0; q < 4; ++q) c[q] = decide_byte<0, 255>(fma(m[w * 4 + q], A, BcM), mq_x, (q & 1) ? kmin2 : kmin);
       // low byte of each decision into one word (three byte permutes)
       sh.idx[lane][h * 8 + w] = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
     }
+    kmin = min(kmin, kmin2);
     bool near = kmin < 2u * mq_x;
     pair_bar(bar);    // B3: full index grid visible
 
