@@ -58,6 +58,18 @@ struct PairShared {
 #endif
 };
 
+// 1/a within 2u (faithful) for normal a in the ranges the status checks admit:
+// the hardware approximation (~2^-22) refined by two Newton steps.  Blocks outside
+// those ranges are marked NEED_EXACT, so their values here do not matter.
+__device__ __forceinline__ double rcp_faithful(double a) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double e = fma(-a, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-a, y, 1.0);
+  return fma(y, e, y);
+}
+
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 // Certified decision on y (see fastpath.cuh::decide): t = y + 1.5*2^20 + 0.5
@@ -261,11 +273,15 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     const double step = 2.0 * smax / 256;      // (:91)
     const uint32_t em = (hi32(smax) >> 20) & 0x7ff;
     if (status == DERR_NONE && (em < 64 || em > 2000)) status = NEED_EXACT;
-    const double inv_step = 1.0 / step;
-    const double A = (1.0 / s) * inv_step;
+    // Faithful reciprocals (within 2u) for the fast-path factors; the margin below
+    // is 2^-41 (1 + L), twice what correctly rounded ones need.
+    const double inv_step = rcp_faithful(step);
+    const double A = rcp_faithful(s) * inv_step;
     const double Bc = -lo * inv_step;
     const double BcM = Bc + kDecideM;  // rounded: <= 2^-33, the extra unit below
-    uint32_t mq_x = margin32(2.2737367544323206e-13 * (1.0 + fabs(lo) / smax));
+    // L = |lo| / s_max enters only the margin: |lo| * inv_step / 128 is within 3u of
+    // it, far inside the bound's >= 2x slack (2^-42 (1 + L) against u (512 + 384 L)).
+    uint32_t mq_x = margin32(4.547473508864641e-13 * (1.0 + fabs(lo) * inv_step * 0.0078125));
     mq_x += mq_x < 0x7FFFFFFFu ? 1u : 0u;
     if (mq_x >= 0x7FFFFFFFu) status = (status == DERR_NONE) ? NEED_EXACT : status;
     // min over decisions of (frac + m) mod 2^32, in two chains (odd / even cells)
@@ -401,9 +417,17 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     const double m_lo = fmax(ad00, step * __hiloint2double((int)gh, 0)) * (1.0 - 2.3e-16) - Ed;
     const double m_hi = fmax(ad00, step * __hiloint2double((int)(gh + 1u), 0)) * (1.0 + 2.3e-16) + Ed;
     if (status == DERR_NONE && (!(m_lo > 4.0 * Ed) || !(m_hi < 4.6e18))) status = NEED_EXACT;
-    double phi = floor((127.0 / m_hi) * (1.0 - 4.5e-16));
+    // No division: 127/m_lo = (127/m_hi) / (1 - x), x = (m_hi - m_lo)/m_hi, is at
+    // most R (1 + x + 2x^2) for x <= 1/2; x is taken from R as (m_hi - m_lo) R / 127.
+    // The computed upper end carries every rounding (<= 14u) and the reference's own
+    // rounding of 127/m (u) inside the factor 1 + 2e-15 (18u); the lower end's factor
+    // 1 - 1e-15 (9u) covers R's 3u, one multiply and the reference's rounding.
+    const double R = 127.0 * rcp_faithful(m_hi);  // within 3u of 127 / m_hi
+    double phi = floor(R * (1.0 - 1e-15));
     phi = phi < 1.0 ? 1.0 : (phi > 255.0 ? 255.0 : phi);
-    double phi_hi = floor((127.0 / m_lo) * (1.0 + 4.5e-16));
+    const double xq = (m_hi - m_lo) * R * 0.007874015748031496;
+    if (status == DERR_NONE && !(xq < 0.25)) status = NEED_EXACT;
+    double phi_hi = floor(R * (1.0 + fma(2.0 * xq, xq, xq)) * (1.0 + 2e-15));
     phi_hi = phi_hi < 1.0 ? 1.0 : (phi_hi > 255.0 ? 255.0 : phi_hi);
     if (status == DERR_NONE && phi != phi_hi) status = NEED_EXACT;
 
