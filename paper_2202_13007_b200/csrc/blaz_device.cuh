@@ -382,6 +382,24 @@ __device__ __forceinline__ bool combine_fast(const RBlock& b1, const RBlock& b2,
   return true;
 }
 
+// Block coordinates (row-major block grid) of t, t + S, t + 2S, ... for a
+// grid-stride loop: one division at the start, then an add with carry per step
+// instead of a 64-bit division per iteration.  bi may run past the grid for
+// lanes beyond the last block; callers clamp those (coords()).
+struct BlockCursor {
+  uint64_t bi, bj, sq, sr;
+  __device__ __forceinline__ BlockCursor(uint64_t t, uint64_t stride, uint64_t bc)
+      : bi(t / bc), bj(t % bc), sq(stride / bc), sr(stride % bc) {}
+  __device__ __forceinline__ void advance(uint64_t bc) {
+    bj += sr;
+    bi += sq;
+    if (bj >= bc) {
+      bj -= bc;
+      ++bi;
+    }
+  }
+};
+
 // ---- SoA global access -------------------------------------------------------
 __device__ __forceinline__ RBlock load_block(const CMat& m, uint64_t t) {
   RBlock b;

@@ -147,12 +147,13 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
   const uint64_t groups = (nb + 31) / 32;
   const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
 
-  for (uint64_t g = (uint64_t)blockIdx.x * (PAIR_WARPS / 2) + pair; g < groups;
-       g += (uint64_t)gridDim.x * (PAIR_WARPS / 2)) {
+  const uint64_t g0 = (uint64_t)blockIdx.x * (PAIR_WARPS / 2) + pair;
+  const uint64_t gstep = (uint64_t)gridDim.x * (PAIR_WARPS / 2);
+  BlockCursor cur(g0 * 32 + lane, gstep * 32, out.bc);
+  for (uint64_t g = g0; g < groups; g += gstep, cur.advance(out.bc)) {
     const uint64_t t = g * 32 + lane;
     const bool valid = t < nb;
-    const uint64_t tt = valid ? t : nb - 1;
-    const uint64_t bi = tt / out.bc, bj = tt % out.bc;
+    const uint64_t bi = valid ? cur.bi : out.br - 1, bj = valid ? cur.bj : out.bc - 1;
     const uint64_t c0 = bj * BD;
     const bool vec = aligned && bi * BD + BD <= rows && c0 + BD <= cols;
 
