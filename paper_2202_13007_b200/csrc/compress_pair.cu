@@ -322,10 +322,10 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
       double oth[4][4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int sft = 8 * (h ? 3 - c : c);
+        const uint32_t sel = 0x4440u | (uint32_t)(h ? 3 - c : c);  // byte col(c) & 3, zero-extended
         int kk[8];
 #pragma unroll
-        for (int u = 0; u < BD; ++u) kk[u] = (int)((wv[u] >> sft) & 0xffu);
+        for (int u = 0; u < BD; ++u) kk[u] = (int)__byte_perm(wv[u], 0u, sel);
         double yo[4], yx[4];
         dct8_int_half(ho, h, kk, yo);
         dct8_int_half(hx, 1 - h, kk, yx);
@@ -439,27 +439,45 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     const bool zero_c = (status == 0x40u);  // constant block: all coefficients 0
     uint8_t* cb = sh.cbytes + lane * 28;
     kmin = 0xFFFFFFFFu;
-    // local rows 0..3, columns 0,1 (both halves): global row r = 4h + ii,
-    // k = 8r + c for r < 2, 14 + r (c = 0) / 20 + r (c = 1) otherwise.
+    // Decisions of local rows 0..3, columns 0,1 (both halves) and, in the upper
+    // half, rows 0,1, columns 2..7; the low byte of each is the coefficient byte.
+    // Keep-set positions (global row r = 4h + ii): k = 8r + c for r < 2,
+    // 14 + r (c = 0) and 20 + r (c = 1) otherwise.  Bytes are packed with PRMT and
+    // stored as words / half-words.
+    uint32_t cbv[4][2];
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const double gv = ii < 2 ? G[ii * 8 + c] : G[16 + (ii - 2) * 2 + c];
         const double t = (h == 0 && ii == 0 && c == 0) ? fma(phi, d00, kDecideM) : fma(gv, ps, kDecideM);
-        const uint32_t byte = decide_byte<-127, 127>(t, mq_c, kmin) & 0xffu;
-        const int r = 4 * h + ii;
-        const int k = r < 2 ? 8 * r + c : (c == 0 ? 14 + r : 20 + r);
-        cb[k] = zero_c ? 0 : (uint8_t)byte;
+        cbv[ii][c] = decide_byte<-127, 127>(t, mq_c, kmin);
       }
-    if (h == 0) {  // rows 0,1, columns 2..7
+    const uint32_t zm = zero_c ? 0u : 0xFFFFFFFFu;
+    auto pack4 = [](uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+      return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+    };
+    if (h == 0) {
+      uint32_t rb[2][8];
 #pragma unroll
-      for (int ii = 0; ii < 2; ++ii)
+      for (int ii = 0; ii < 2; ++ii) {
+        rb[ii][0] = cbv[ii][0];
+        rb[ii][1] = cbv[ii][1];
 #pragma unroll
-        for (int c = 2; c < 8; ++c) {
-          const uint32_t byte = decide_byte<-127, 127>(fma(G[ii * 8 + c], ps, kDecideM), mq_c, kmin) & 0xffu;
-          cb[8 * ii + c] = zero_c ? 0 : (uint8_t)byte;
-        }
+        for (int c = 2; c < 8; ++c) rb[ii][c] = decide_byte<-127, 127>(fma(G[ii * 8 + c], ps, kDecideM), mq_c, kmin);
+      }
+      uint32_t* cw = reinterpret_cast<uint32_t*>(cb);
+#pragma unroll
+      for (int ii = 0; ii < 2; ++ii) {
+        cw[2 * ii] = pack4(rb[ii][0], rb[ii][1], rb[ii][2], rb[ii][3]) & zm;
+        cw[2 * ii + 1] = pack4(rb[ii][4], rb[ii][5], rb[ii][6], rb[ii][7]) & zm;
+      }
+      *reinterpret_cast<uint16_t*>(cb + 16) = (uint16_t)(__byte_perm(cbv[2][0], cbv[3][0], 0x0040) & zm);
+      *reinterpret_cast<uint16_t*>(cb + 22) = (uint16_t)(__byte_perm(cbv[2][1], cbv[3][1], 0x0040) & zm);
+    } else {
+      *reinterpret_cast<uint16_t*>(cb + 18) = (uint16_t)(__byte_perm(cbv[0][0], cbv[1][0], 0x0040) & zm);
+      *reinterpret_cast<uint16_t*>(cb + 20) = (uint16_t)(__byte_perm(cbv[2][0], cbv[3][0], 0x0040) & zm);
+      *reinterpret_cast<uint32_t*>(cb + 24) = pack4(cbv[0][1], cbv[1][1], cbv[2][1], cbv[3][1]) & zm;
     }
     near |= kmin < 2u * mq_c;
     if (h == 1) sh.nearL[lane] = near ? 1u : 0u;
