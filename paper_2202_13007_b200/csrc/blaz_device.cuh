@@ -390,6 +390,11 @@ struct BlockCursor {
   uint64_t bi, bj, sq, sr;
   __device__ __forceinline__ BlockCursor(uint64_t t, uint64_t stride, uint64_t bc)
       : bi(t / bc), bj(t % bc), sq(stride / bc), sr(stride % bc) {}
+  // stride quotient / remainder precomputed by the host
+  __device__ __forceinline__ BlockCursor(uint64_t t, uint64_t bc, uint64_t sq_, uint64_t sr_)
+      : bi(t / bc), sq(sq_), sr(sr_) {
+    bj = t - bi * bc;
+  }
   __device__ __forceinline__ void advance(uint64_t bc) {
     bj += sr;
     bi += sq;

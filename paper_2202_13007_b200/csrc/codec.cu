@@ -7,6 +7,10 @@
 #include "fastpath.cuh"  // FastParams, NEED_EXACT
 #include "launch.h"
 
+#ifndef DEC_GRID_PER_SM
+#define DEC_GRID_PER_SM 64
+#endif
+
 namespace blz {
 
 // Edge-replicated tile load (H/matrix.hpp:72-84).
@@ -103,9 +107,9 @@ __global__ void __launch_bounds__(128) k_dequantize(const Basis B, CMat in, doub
   }
 }
 
-static unsigned grid_for(uint64_t n, unsigned threads, int sms) {
+static unsigned grid_for(uint64_t n, unsigned threads, int sms, unsigned per_sm = 64) {
   const uint64_t want = (n + threads - 1) / threads;
-  const uint64_t cap = (uint64_t)sms * 64;
+  const uint64_t cap = (uint64_t)sms * per_sm;
   return (unsigned)(want < cap ? (want ? want : 1) : cap);
 }
 
@@ -137,7 +141,7 @@ cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in
 
 cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
-  const unsigned g = grid_for(in.nb(), 128, c.sm_count);
+  const unsigned g = grid_for(in.nb(), 128, c.sm_count, DEC_GRID_PER_SM);
   if (c.basis_sym && !c.exact_only)  // exact mode keeps the plain product-per-term kernel
     k_decompress<true><<<g, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
   else

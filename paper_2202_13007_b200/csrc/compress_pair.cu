@@ -39,6 +39,9 @@ struct Butterfly {
   double c2[2][8];  // pass-2 constants per half; the lower half's odd ones negated
 };
 
+#ifndef CP_GRID_MULT
+#define CP_GRID_MULT 128  // CTAs per SM in the grid (8 resident): short-lived CTAs desynchronise the pairs
+#endif
 #ifndef CP_COLSPLIT
 #define CP_COLSPLIT 1
 #endif
@@ -136,7 +139,7 @@ __device__ __forceinline__ void dct8_f64(const double (&c)[8], const double (&z)
 __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     k_compress_pair(const FastParams P, const Butterfly W, const double* __restrict__ dense, uint64_t rows,
                     uint64_t cols, uint64_t ld, CMat out, uint64_t* __restrict__ wl,
-                    unsigned long long* __restrict__ wl_count) {
+                    unsigned long long* __restrict__ wl_count, uint64_t step_q, uint64_t step_r) {
   __shared__ PairShared shared[PAIR_WARPS / 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
 
   const uint64_t g0 = (uint64_t)blockIdx.x * (PAIR_WARPS / 2) + pair;
   const uint64_t gstep = (uint64_t)gridDim.x * (PAIR_WARPS / 2);
-  BlockCursor cur(g0 * 32 + lane, gstep * 32, out.bc);
+  BlockCursor cur(g0 * 32 + lane, out.bc, step_q, step_r);
   for (uint64_t g = g0; g < groups; g += gstep, cur.advance(out.bc)) {
     const uint64_t t = g * 32 + lane;
     const bool valid = t < nb;
@@ -159,25 +162,33 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
 
     // ---- own rows + (lower half) row 3, original values, edge-replicated ---
     double m[32], up[8];
-    {
+    if (vec) {  // whole tile inside: one row pointer, rows at +ld
+      const double* p = dense + (bi * BD + 4 * h) * ld + c0;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        if (i == 4 && h == 0) break;
+        const double2* row = reinterpret_cast<const double2*>(i < 4 ? p + i * ld : p - ld);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 x = __ldg(row + q);
+          if (i < 4) {
+            m[i * BD + 2 * q] = x.x;
+            m[i * BD + 2 * q + 1] = x.y;
+          } else {
+            up[2 * q] = x.x;
+            up[2 * q + 1] = x.y;
+          }
+        }
+      }
+    } else {    // edge tile: clamped rows / columns (edge replication)
       const uint64_t r0 = bi * BD + 4 * h;
 #pragma unroll
       for (int i = 0; i < 5; ++i) {
         if (i == 4 && h == 0) break;
         const uint64_t r = (i < 4) ? min(r0 + i, rows - 1) : min(bi * BD + 3, rows - 1);
         double v[8];
-        if (vec) {
-          const double2* row = reinterpret_cast<const double2*>(dense + r * ld + c0);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double2 x = __ldg(row + q);
-            v[2 * q] = x.x;
-            v[2 * q + 1] = x.y;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < BD; ++j) v[j] = __ldg(dense + r * ld + min(c0 + j, cols - 1));
-        }
+        for (int j = 0; j < BD; ++j) v[j] = __ldg(dense + r * ld + min(c0 + j, cols - 1));
 #pragma unroll
         for (int j = 0; j < BD; ++j) {
           if (i < 4) m[i * BD + j] = v[j];
@@ -524,9 +535,11 @@ cudaError_t launch_compress_pair(const LaunchCtx& c, const FastParams& P, const 
   }
   const uint64_t groups = (out.nb() + 31) / 32;
   const uint64_t want = (groups + PAIR_WARPS / 2 - 1) / (PAIR_WARPS / 2);
-  const uint64_t cap = (uint64_t)c.sm_count * 32;
+  const uint64_t cap = (uint64_t)c.sm_count * CP_GRID_MULT;
   const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
-  k_compress_pair<<<g, PAIR_WARPS * 32, 0, c.stream>>>(P, W, dense, rows, cols, ld, out, c.wl, c.wl_count);
+  const uint64_t stride = (uint64_t)g * (PAIR_WARPS / 2) * 32;  // blocks per grid-stride step
+  k_compress_pair<<<g, PAIR_WARPS * 32, 0, c.stream>>>(P, W, dense, rows, cols, ld, out, c.wl, c.wl_count,
+                                                       stride / out.bc, stride % out.bc);
   ++*c.launches;
   return cudaGetLastError();
 }
