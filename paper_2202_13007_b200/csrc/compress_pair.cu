@@ -234,7 +234,11 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     // selects per cell, the high word's sign cleared by the select's |.|.
     // Two independent chains (even / odd cells), merged at the end: the maximum
     // is exact in any order, and the split halves the compare-select latency.
-    uint32_t zmin = 0xFFFFFFFFu;
+    // zero test on the high words only, as floats (|hi| is monotone as a float bit
+    // pattern; NaN patterns, |delta| >= 2^1017, are nonzero and ignored by fminf).
+    // A zero high word with a nonzero low word (subnormal delta) only sends the
+    // block through the exact count below.
+    float zminf = 3.0e38f;
     float amax_h[2] = {0.0f, 0.0f};
     uint32_t amax_l[2] = {0u, 0u};
 #pragma unroll
@@ -243,8 +247,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
       const bool gt = fabs(m[k]) > __hiloint2double(__float_as_int(amax_h[c]), (int)amax_l[c]);
       amax_h[c] = gt ? fabsf(__int_as_float((int)hi32(m[k]))) : amax_h[c];
       amax_l[c] = gt ? lo32(m[k]) : amax_l[c];
-      const uint32_t zk = (hi32(m[k]) & 0x7FFFFFFFu) | lo32(m[k]);
-      zmin = min(zmin, (k == 0 && h == 0) ? 0xFFFFFFFFu : zk);
+      zminf = (k == 0 && h == 0) ? zminf : fminf(zminf, fabsf(__int_as_float((int)hi32(m[k]))));
     }
     {
       const bool gt = __hiloint2double(__float_as_int(amax_h[1]), (int)amax_l[1]) >
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     }
     amax = __hiloint2double(__float_as_int(amax_h[0]), (int)amax_l[0]);
     int nz = 32 - (h == 0);
-    if (zmin == 0) {  // some zero deltas (rare on real data): count them
+    if (zminf == 0.0f) {  // some zero deltas (rare on real data): count them
       nz = 0;
 #pragma unroll
       for (int k = 0; k < 32; ++k) nz += fabs(m[k]) > 0.0;
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
     // ---- pass 2 (own rows), max|G| and the retained entries ---------------
     // Row ii of Z in butterfly form: z[j] + z[7-j] = own[j] + B[j] and
     // z[j] - z[7-j] = +-(own[j] - B[j]) (sign - for h = 1, folded into c2[1]).
-    uint32_t gh = 0;
+    float ghf = 0.0f;  // max over |G| high words, as a float (|G| < 2^12: never a NaN pattern)
     double G[20];
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii) {
@@ -376,8 +379,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
       dct8_f64(W.c2[h], z, gr);
 #pragma unroll
       for (int j = 0; j < BD; ++j) {
-        const uint32_t a = hi32(gr[j]) & 0x7FFFFFFFu;
-        gh = (ii == 0 && j == 0 && h == 0) ? gh : max(gh, a);
+        ghf = (ii == 0 && j == 0 && h == 0) ? ghf : fmaxf(ghf, fabsf(__int_as_float((int)hi32(gr[j]))));
         if (ii < 2) G[ii * 8 + j] = gr[j];
         else if (j < 2) G[16 + (ii - 2) * 2 + j] = gr[j];
       }
@@ -417,6 +419,9 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
         else if (j < 2) G[16 + (ii - 2) * 2 + j] = gr[j];
       }
     }
+#endif
+#if CP_COLSPLIT
+    uint32_t gh = (uint32_t)__float_as_int(ghf);
 #endif
     sh.gh[h][lane] = gh;
     if (h == 0) sh.d00[lane] = fma(step, G[0], lo * P.ss00);
