@@ -243,6 +243,50 @@ def test_fast_path_matches_exact_and_oracle(port):
     assert used_exact < 0.25 * n, used_exact
 
 
+def _extreme_tiles(n_each=256, seed=11):
+    """Blocks at the edges of binary64: subnormal and near-2^-1021 deltas (where
+    halving rounds), a subnormal next to a unit delta, 5e307 steps, signed zeros
+    with one subnormal."""
+    rng = np.random.default_rng(seed)
+    tiles = []
+    tiles.append(rng.integers(-1000, 1000, size=(n_each, 8, 8)).astype(np.float64) * 5e-324)
+    tiles.append(rng.normal(size=(n_each, 8, 8)) * 1e-306)
+    mixed = np.zeros((n_each, 8, 8))
+    mixed[:, 2, 3] = 3e-310 * rng.integers(1, 9, size=n_each)
+    mixed[:, 5, 6] = rng.normal(size=n_each)
+    tiles.append(mixed)
+    huge = np.zeros((n_each, 8, 8))
+    huge[:, 0, 1] = 5e307 * rng.choice([-1.0, 1.0], size=n_each)
+    huge[:, 4, 4] = rng.normal(size=n_each)
+    tiles.append(huge)
+    signed_zero = np.where(rng.random((n_each, 8, 8)) < 0.5, -0.0, 0.0)
+    signed_zero[:, 7, 7] = 1e-320
+    tiles.append(signed_zero)
+    return np.concatenate(tiles)
+
+
+def test_fast_path_extreme_magnitudes(port):
+    """Subnormal and near-2^-1021 deltas, zero tests on subnormal high words,
+    overflowing sums: the fast path must certify or hand over every block, so
+    fast == exact == oracle on all of them."""
+    tiles = _extreme_tiles()
+    n = tiles.shape[0]
+    dense = torch.from_numpy(tiles.reshape(n * 8, 8)).cuda()
+    ctx = dev.context()
+    fast = dev.compress(dense)
+    dev.sync()
+    ctx.set_mode(blz.MODE_EXACT)
+    try:
+        exact = dev.compress(dense)
+        dev.sync()
+    finally:
+        ctx.set_mode(blz.MODE_DEFAULT)
+    hf, he = fast.to_host().blocks.reshape(-1), exact.to_host().blocks.reshape(-1)
+    want = port.compress_matrix(tiles.reshape(n * 8, 8)).reshape(-1)
+    assert blocks_equal(he, want), block_diff_report(he, want)
+    assert blocks_equal(hf, want), block_diff_report(hf, want)
+
+
 def test_decompress_shared_products_match_plain_kernel(port):
     """The default decompress shares the products of bitwise-repeated basis
     entries; exact mode runs one product per term.  Both equal the oracle."""
