@@ -42,6 +42,9 @@ struct Butterfly {
 #ifndef CP_GRID_MULT
 #define CP_GRID_MULT 128  // CTAs per SM in the grid (8 resident): short-lived CTAs desynchronise the pairs
 #endif
+#ifndef CP_SIMD_P1
+#define CP_SIMD_P1 1
+#endif
 #ifndef CP_COLSPLIT
 #define CP_COLSPLIT 1
 #endif
@@ -119,6 +122,25 @@ __device__ __forceinline__ void dct8_int_half(const double (&hc)[11], int h, con
   y[1] = fma(hc[3], d0, fma(hc[4], d1, fma(hc[5], d2, hc[6] * d3)));
   y[2] = fma(hc[1], e0, hc[2] * e1);
   y[3] = fma(hc[7], d0, fma(hc[8], d1, fma(hc[9], d2, hc[10] * d3)));
+}
+
+// The FP64 part of dct8_int_half on converted butterfly values (pq = p + q for
+// the upper outputs, p - q for the lower ones): the same operations, same order.
+__device__ __forceinline__ void dct8_f64_half(const double (&hc)[11], double pq, const double (&d)[4], double e0,
+                                              double e1, double (&y)[4]) {
+  y[0] = hc[0] * pq;
+  y[1] = fma(hc[3], d[0], fma(hc[4], d[1], fma(hc[5], d[2], hc[6] * d[3])));
+  y[2] = fma(hc[1], e0, hc[2] * e1);
+  y[3] = fma(hc[7], d[0], fma(hc[8], d[1], fma(hc[9], d[2], hc[10] * d[3])));
+}
+
+// Signed 16-bit lane l of w as a double (I2F.F64.S16 with a half selector).
+__device__ __forceinline__ double s16_lane_to_f64(uint32_t w, int l) {
+  unsigned short lo, hi;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w));
+  double d;
+  asm("cvt.rn.f64.s16 %0, %1;" : "=d"(d) : "h"(l ? hi : lo));
+  return d;
 }
 
 // All 8 outputs of the transform of a double vector z[0..7].
@@ -334,6 +356,48 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
 #pragma unroll
       for (int u = 0; u < BD; ++u) wv[u] = sh.idx[lane][u * 2 + h];
       double oth[4][4];
+#if CP_SIMD_P1
+      // Two columns per pass through the integer butterflies: 16-bit lanes of
+      // one register (VIADD.16x2 / IADD3), each difference formed with a bias that
+      // keeps the lower lane from borrowing and removed per lane; the lanes then
+      // convert with I2F.F64.S16 (.H0 / .H1).  The integers are the same, so every
+      // double is the one the scalar version computed.
+#pragma unroll
+      for (int pr = 0; pr < 2; ++pr) {
+        const uint32_t i0 = (uint32_t)(h ? 3 - 2 * pr : 2 * pr), i1 = (uint32_t)(h ? 2 - 2 * pr : 2 * pr + 1);
+        const uint32_t sel = 0x4040u | (i1 << 8) | i0;  // bytes col(c0), col(c1) into lanes 0, 1
+        uint32_t kw[8];
+#pragma unroll
+        for (int u = 0; u < BD; ++u) kw[u] = __byte_perm(wv[u], 0u, sel);
+        uint32_t sw[4], dw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          sw[j] = kw[j] + kw[7 - j];
+          dw[j] = __vadd2(kw[j] - kw[7 - j] + 0x01000100u, 0xFF00FF00u);
+        }
+        const uint32_t e0w = __vadd2(sw[0] - sw[3] + 0x02000200u, 0xFE00FE00u);
+        const uint32_t e1w = __vadd2(sw[1] - sw[2] + 0x02000200u, 0xFE00FE00u);
+        const uint32_t pw = sw[0] + sw[3], qw = sw[1] + sw[2];
+        const uint32_t ppq = pw + qw, pmq = __vadd2(pw - qw + 0x04000400u, 0xFC00FC00u);
+#pragma unroll
+        for (int l = 0; l < 2; ++l) {
+          double d[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) d[j] = s16_lane_to_f64(dw[j], l);
+          const double e0 = s16_lane_to_f64(e0w, l), e1 = s16_lane_to_f64(e1w, l);
+          const double vpq = s16_lane_to_f64(ppq, l), vmq = s16_lane_to_f64(pmq, l);
+          double yo[4], yx[4];
+          dct8_f64_half(ho, h ? vmq : vpq, d, e0, e1, yo);
+          dct8_f64_half(hx, h ? vpq : vmq, d, e0, e1, yx);
+          const int c = 2 * pr + l;
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii) {
+            own[ii][c] = yo[ii];
+            oth[ii][c] = yx[ii];
+          }
+        }
+      }
+#else
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint32_t sel = 0x4440u | (uint32_t)(h ? 3 - c : c);  // byte col(c) & 3, zero-extended
@@ -349,6 +413,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
           oth[ii][c] = yx[ii];
         }
       }
+#endif
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
