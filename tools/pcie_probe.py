@@ -36,3 +36,27 @@ def both():
 
 tb = t(both)
 print(f"H2D {gb / th:.1f} GB/s  D2H {gb / td:.1f} GB/s  both directions at once {2 * gb / tb:.1f} GB/s total")
+
+
+def d2h_split(k):
+    ss = [torch.cuda.Stream() for _ in range(k)]
+    step = n // k
+
+    def f():
+        for i, s_ in enumerate(ss):
+            with torch.cuda.stream(s_):
+                h2[i * step:(i + 1) * step].copy_(d[i * step:(i + 1) * step], non_blocking=True)
+    return f
+
+
+def d2h_chunks(chunk):
+    def f():
+        for i in range(0, n, chunk):
+            h2[i:i + chunk].copy_(d[i:i + chunk], non_blocking=True)
+    return f
+
+
+for k in (2, 4):
+    print(f"D2H over {k} streams: {gb / t(d2h_split(k)):.1f} GB/s")
+for c in (2 ** 20, 2 ** 23):
+    print(f"D2H in {c * 8 >> 20} MiB chunks: {gb / t(d2h_chunks(c)):.1f} GB/s")
