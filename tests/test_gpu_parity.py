@@ -183,6 +183,36 @@ def test_addsub_rounding_ties_and_large_weights(port):
     assert np.any(phis % 2 == 0)
 
 
+def _extreme_records(n, seed):
+    rng = np.random.default_rng(seed)
+    rec = np.zeros(n, dtype=blz.BLOCK_DTYPE)
+    firsts = np.array([0.0, -0.0, 1e-310, -3e-320, 1e300, -1e300, 1.0, -2.5])
+    slopes = np.array([0.0, 5e-324, 1e-310, 1e-300, 1.0, -1.0, -1.0000001, 1e300, -3e-5])
+    rec["first"] = np.where(rng.random(n) < 0.5, firsts[rng.integers(0, 8, n)], rng.normal(size=n))
+    rec["slope"] = np.where(rng.random(n) < 0.7, slopes[rng.integers(0, 9, n)], rng.normal(size=n))
+    rec["scale_factor"] = np.array([1, 2, 3, 127, 128, 254, 255], dtype=np.uint8)[rng.integers(0, 7, n)]
+    rec["coeffs"] = rng.integers(-127, 128, size=(n, 28)).astype(np.int8)
+    return rec
+
+
+def test_records_with_extreme_values(port):
+    """add / sub / scale / decompress on records with signed zeros, subnormal and
+    huge first values and slopes, cancelling slopes (the dense fallback and the
+    huge-weight rounding) and every scale-factor class: equal to the oracle."""
+    rows, cols = 64, 96
+    nb = (rows // 8) * (cols // 8)
+    ra, rb = _extreme_records(nb, 1), _extreme_records(nb, 2)
+    A, B = blz.CompressedMatrix(rows, cols, ra), blz.CompressedMatrix(rows, cols, rb)
+    for got, want in [(blz.mat_add(A, B).blocks, port.mat_add(ra, rb)),
+                      (blz.mat_sub(A, B).blocks, port.mat_sub(ra, rb)),
+                      (blz.mat_scale(A, -2.5).blocks, port.mat_scale(ra, -2.5)),
+                      (blz.mat_scale(A, 1e10).blocks, port.mat_scale(ra, 1e10))]:
+        assert blocks_equal(got, want), block_diff_report(got, want)
+    got = blz.decompress_matrix(A)
+    want = port.decompress_matrix(ra.reshape(-1), rows, cols)
+    assert np.array_equal(bits(got), bits(want))
+
+
 def test_gemm_fused_mode_tolerance(port):
     a = W.smooth_field(64, 96, seed=3).numpy()
     b = W.smooth_field(96, 40, seed=4).numpy()
