@@ -219,6 +219,9 @@ __device__ __forceinline__ double dequant(int c, double phi, double r) {
 // t(4,4) = -t(4,2) (checked on the host, analyse_basis).  Equal factors give
 // equal (or exactly negated) rounded products, so those products are formed
 // once; every sum keeps the reference's order.
+#ifndef DEC_DQSEL
+#define DEC_DQSEL 0  // the output select alone yields the +0.0 grid for s == 0
+#endif
 template <bool SLOPES_ONLY, bool SYM = false, class Emit>
 __device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basis& B, Emit&& emit) {
   const double s = b.s;
@@ -230,7 +233,7 @@ __device__ __forceinline__ void decompress_rows_impl(const RBlock& b, const Basi
   if (b.phi - 1u < 255u) {
     const double r = 1.0 / fphi;
 #pragma unroll
-    for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : dequant_d(i8_byte_to_f64(b.c[k >> 2], k & 3), fphi, r);
+    for (int k = 0; k < KEPT; ++k) dq[k] = DEC_DQSEL && zero ? 0.0 : dequant_d(i8_byte_to_f64(b.c[k >> 2], k & 3), fphi, r);
   } else {
 #pragma unroll
     for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : (double)get_coeff(b.c, k) / fphi;
