@@ -11,9 +11,15 @@ pipeline on HBM-resident dense inputs:
 summed over ranks (weak scaling: every rank owns its own 16384x16384 pair, the
 ops shard by block-rows with no communication).  Per-op blocks/s, GB/s and HBM
 fractions are in `ops`; `roofline` is for the dominant kernel (decompress).
+`configs` holds BASELINE configs 2-4 block-row sharded over the ranks (strong
+scaling, with their collectives) and the fused-GEMM parity statistics.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg1|cfg0|cfg3] [--no-e2e] [--no-cpu-baseline]
+                    [--config cfg1|cfg0] [--no-e2e] [--no-cpu-baseline] [--no-extras]
+
+--gpus N without torchrun re-executes itself under torchrun (one rank per GPU).
+--impl reference times the reference's own CPU implementation (oracle/_ref) on
+the whole config-1 workload on all host cores, without importing our package.
 """
 from __future__ import annotations
 
@@ -139,20 +145,31 @@ def barrier(world):
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference (oracle/_ref) or the oracle port on host cores
 # ---------------------------------------------------------------------------
-def cpu_reference_step_fn(cfg, sample_rows, threads):
-    """Returns (kind, fn) where fn() runs one config step on a block-row sample and returns seconds."""
-    import torch
+def load_workloads():
+    """paper_2202_13007_b200/workloads.py loaded by path: the generators only need
+    torch, and loading them this way keeps the package (and its CUDA library)
+    out of the reference arm's process."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_blz_workloads", os.path.join(ROOT, "paper_2202_13007_b200", "workloads.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
+
+def cpu_reference_step_fn(cfg, sample_rows, threads):
+    """Returns (kind, threads, fn) where fn() runs one config step on the first
+    `sample_rows` rows of the workload and returns seconds."""
     from oracle import oracle as O
-    from paper_2202_13007_b200 import workloads as W
+    W = load_workloads()
     rows, cols = sample_rows, cfg["cols"]
     a = W.make(cfg["gen"], rows, cols, seed=1).numpy()
     b = W.make(cfg["gen"], rows, cols, seed=2).numpy()
-    del torch
     if O.ref_available():
         r = O.ref()
         ha = r.dense_new(a.ctypes.data, rows, cols)
         hb = r.dense_new(b.ctypes.data, rows, cols)
+        del a, b
 
         def step():
             t0 = time.perf_counter()
@@ -189,31 +206,66 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+def reference_matmul_full(n, gen, seeds, threads):
+    """The reference's mat_mul on the whole n^3 problem, once (compressed in and out)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None
+    W = load_workloads()
+    r = O.ref()
+    hs = []
+    for sd in seeds:
+        d = W.make(gen, n, n, seed=sd).numpy()
+        hs.append(r.dense_new(d.ctypes.data, n, n))
+        del d
+    ca, cb = r.h_compress(hs[0], threads), r.h_compress(hs[1], threads)
+    for h in hs:
+        r.dense_free(h)
+    t0 = time.perf_counter()
+    cc = r.h_mul(ca, cb, threads)
+    dt = time.perf_counter() - t0
+    for h in (ca, cb, cc):
+        r.cm_free(h)
+    return {"workload": f"{n}^3 compressed matmul, {gen} data (reference mat_mul, whole problem, once)",
+            "ms": round(dt * 1e3, 1), "tflops": 2.0 * n ** 3 / dt / 1e12, "cores": threads, "kind": "reference"}
+
+
 def run_reference_arm(args, cfg, rank, world):
-    """--impl reference: the reference's own CPU implementation on host cores."""
+    """--impl reference: the reference's own CPU implementation (oracle/_ref, the
+    reference headers compiled unmodified) on all host cores, over the SAME
+    config-1 workload as our arm (both 16384^2 matrices, every block).  Only
+    rank 0 works under torchrun; this process never imports the package."""
     if rank != 0:
         return None
     threads = host_threads()
-    sample_rows = args.ref_sample_rows
-    kind, used_threads, step = cpu_reference_step_fn(cfg, sample_rows, threads)
-    blocks = (sample_rows // 8) * ((cfg["cols"] + 7) // 8)
+    rows = cfg["rows"] if args.ref_sample_rows <= 0 else min(cfg["rows"], args.ref_sample_rows)
+    kind, used_threads, step = cpu_reference_step_fn(cfg, rows, threads)
+    blocks = ((rows + 7) // 8) * ((cfg["cols"] + 7) // 8)
     for _ in range(args.warmup):
         step()
     times = [step() for _ in range(args.steps)]
     total = sum(times)
     value = blocks * args.steps / total
-    sample = (f"{sample_rows}x{cfg['cols']} block-row slice of {args.config} "
-              f"({blocks} blocks/step), reference threads={used_threads}")
+    whole = rows == cfg["rows"]
+    sample = (f"{'the whole' if whole else 'a block-row slice of the'} {rows}x{cfg['cols']} {args.config} "
+              f"workload ({blocks} blocks/step), reference threads={used_threads}")
     line = {
         "metric": "cfg1 pipeline 8x8 blocks/s (compress 2, add, sub, scale, decompress 3)",
         "value": value, "unit": "blocks/s", "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded per-block quadratics, BASELINE cfg1 distribution)",
-        "config": {"workload": args.config, "rows": cfg["rows"], "cols": cfg["cols"], "sample_rows": sample_rows},
+        "data": "synthetic (seeded per-block quadratics, BASELINE cfg1 distribution; CPU generator)",
+        "config": {"workload": args.config, "rows": cfg["rows"], "cols": cfg["cols"],
+                   "blocks_per_matrix": blocks, "timed_rows": rows, "same_config": whole},
         "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": used_threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_extras and args.cfg3_size > 0:
+        mm = reference_matmul_full(args.cfg3_size, "smooth", (21, 22), threads)
+        if mm is not None:
+            line["configs"] = {"cfg3": mm}
+    # the reference arm runs the reference alone: our package (and its CUDA library) stays unloaded
+    assert not any(m.startswith("paper_2202_13007_b200") for m in sys.modules), "reference arm imported the package"
     return line
 
 
@@ -364,164 +416,41 @@ def run_ours(args, cfg, rank, world, local):
             line["cpu_baseline"] = cpu_baseline(args, cfg)
     del A, B, cA, cB, cS, cD, cK, oS, oD, oK
     torch.cuda.empty_cache()
-    if not args.no_extras and world == 1:
-        extras = run_extras(args)
+    if not args.no_extras:
+        extras = run_extras(args, rank, world)
         if line is not None:
             line["configs"] = extras
     return line
 
 
-def _chunked_compress(gen, rows, cols, seed, chunk_rows=8192):
-    """Compresses a rows x cols matrix generated chunk by chunk (bounded memory);
-    returns the DeviceCMat and the dense rows of chunk 0 (for parity sampling)."""
-    import torch
-
-    from paper_2202_13007_b200 import device as dev
-    from paper_2202_13007_b200 import workloads as W
-    full = dev.DeviceCMat(rows, cols)
-    bc = (cols + 7) // 8
-    first_rows = None
-    for r0 in range(0, rows, chunk_rows):
-        nr = min(chunk_rows, rows - r0)
-        if gen == "smooth":
-            d = W.smooth_field(nr, cols, seed, device="cuda", row0=r0)
-        else:
-            d = W.make(gen, nr, cols, seed + r0, device="cuda")
-        part = dev.compress(d)
-        b0, b1 = (r0 // 8) * bc, (r0 // 8) * bc + part.nblocks
-        full.first[b0:b1].copy_(part.first)
-        full.slope[b0:b1].copy_(part.slope)
-        full.coeffs[b0:b1].copy_(part.coeffs)
-        full.scale[b0:b1].copy_(part.scale)
-        if r0 == 0:
-            first_rows = d[:64].cpu().numpy()
-        del d, part
-    torch.cuda.synchronize()
-    return full, first_rows
-
-
-def _time(fn, reps, warm=1):
+def _time_dist(fn, reps, world, warm=1):
+    """Device ms per call of fn(), after `warm` calls: CUDA events on the launching
+    stream between barriers, max over ranks."""
     import torch
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
+    barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
         fn()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
-
-
-def run_extras(args):
-    """Configs 2, 3 and (one GPU of) 4 of BASELINE.json (reported beside the cfg1 headline)."""
-    import numpy as np
-    import torch
-
-    from paper_2202_13007_b200 import device as dev
-    out = {}
-    fp64_peak = 36.6  # TFLOP/s, DMMA/DFMA measured (profiles/r01_fp64_peaks.txt)
-    # ---- config 2: row dots + Frobenius of two 65536^2 smooth fields -------------------
-    n2 = args.cfg2_size
-    A, a_rows = _chunked_compress("smooth", n2, n2, 11)
-    B, b_rows = _chunked_compress("smooth", n2, n2, 12)
-    r_holder = {}
-
-    def frob():
-        r_holder["r"], r_holder["t"] = dev.frobenius(A, B)
-    ms = _time(frob, reps=args.extra_reps)
-    nb2 = A.nblocks
-    rec = {"workload": f"cfg2 rowdot+frobenius {n2}x{n2} (smooth fields)", "ms": round(ms, 3),
-           "value": nb2 / (ms * 1e-3), "unit": "block pairs/s",
-           "fp64_note": "exact: two reference-order decompressions per block pair (~3.4k FP64 ops) + serial row chains"}
-    if not args.no_parity:
-        from oracle import oracle as O
-        port = O.port()
-        bc = (n2 + 7) // 8
-        ha, hb = A.to_host(), B.to_host()
-        want = port.rowdot(ha.blocks[:8], hb.blocks[:8], 64, n2)
-        got = r_holder["r"][:64].cpu().numpy()
-        rec["parity"] = {"sampled_rows": 64, "bit_exact": bool(np.array_equal(got.view(np.uint64), want.view(np.uint64)))}
-        del ha, hb
-    if not args.no_cpu_baseline:
-        rec["cpu_baseline"] = cpu_baseline_rowdot(a_rows, b_rows, n2)
-    out["cfg2"] = rec
-    del A, B, r_holder
-    torch.cuda.empty_cache()
-    # ---- config 3: compressed matmul 8192^3 ------------------------------------------------
-    n3 = args.cfg3_size
-    A, a_rows = _chunked_compress("smooth", n3, n3, 21)
-    B, _ = _chunked_compress("smooth", n3, n3, 22)
-    C = dev.DeviceCMat(n3, n3)
-    scratch = dev.matmul_scratch(A, B)
-    flops = 2.0 * n3 ** 3
-    rec = {"workload": f"cfg3 compressed matmul {n3}^3 (compressed in, compressed out)"}
-    for mode, name in ((0, "exact"), (1, "fused_dmma")):
-        ms = _time(lambda: dev.matmul(A, B, mode=mode, out=C, scratch=scratch), reps=args.extra_reps)
-        tf = flops / (ms * 1e-3) / 1e12
-        rec[name] = {"ms": round(ms, 3), "tflops": round(tf, 2), "frac_fp64_peak": round(tf / fp64_peak, 3)}
-    rec["exact"]["note"] = "DMUL+DADD in the reference's order: capped at 50% of the FP64 FMA peak"
-    rec["fused_dmma"]["note"] = "FP64 tensor cores; = ascending-k FMA chain; tolerance parity"
-    if not args.no_parity:
-        from oracle import oracle as O
-        port = O.port()
-        dev.matmul(A, B, mode=0, out=C, scratch=scratch)
-        # row block 0 of C vs the oracle (A's first block-row against all of B)
-        ha, hb = A.to_host(), B.to_host()
-        want = port.mat_mul(ha.blocks[:1], 8, n3, hb.blocks, n3, n3)
-        hc = C.to_host().blocks[:1]
-        same = all(np.array_equal(np.ascontiguousarray(hc[f]).view(np.uint8), np.ascontiguousarray(want[f]).view(np.uint8))
-                   for f in ("first", "slope", "scale_factor", "coeffs"))
-        rec["parity"] = {"sampled_block_rows": 1, "exact_mode_bit_exact": bool(same)}
-        del ha, hb
-    if not args.no_cpu_baseline:
-        rec["cpu_baseline"] = cpu_baseline_matmul(a_rows, n3)
-    out["cfg3"] = rec
-    del A, B, C, scratch
-    torch.cuda.empty_cache()
-    # ---- config 4 (one GPU of the sharded case): rough-data matmul 32768^3 --------------
-    n4 = args.cfg4_size
-    if n4 > 0:
-        A, a_rows = _chunked_compress("rough", n4, n4, 41)
-        B, _ = _chunked_compress("rough", n4, n4, 42)
-        C = dev.DeviceCMat(n4, n4)
-        scratch = dev.matmul_scratch(A, B)
-        flops = 2.0 * n4 ** 3
-        rec = {"workload": f"cfg4 compressed matmul {n4}^3, rough U[-1,1] data, one GPU (compressed in and out)"}
-        for mode, name in ((1, "fused_dmma"), (0, "exact")):
-            ms = _time(lambda: dev.matmul(A, B, mode=mode, out=C, scratch=scratch), reps=1)
-            tf = flops / (ms * 1e-3) / 1e12
-            rec[name] = {"ms": round(ms, 1), "tflops": round(tf, 2), "frac_fp64_peak": round(tf / fp64_peak, 3)}
-        if not args.no_parity:  # C is the exact-mode result (last run)
-            from oracle import oracle as O
-            if O.ref_available():
-                r = O.ref()
-                ha, hb = A.to_host(), B.to_host()
-                want = r.mat_mul(ha.blocks[:1], 8, n4, hb.blocks, n4, n4, host_threads())
-                hc = C.to_host().blocks[:1]
-                same = all(np.array_equal(np.ascontiguousarray(hc[f]).view(np.uint8),
-                                          np.ascontiguousarray(want[f]).view(np.uint8))
-                           for f in ("first", "slope", "scale_factor", "coeffs"))
-                rec["parity"] = {"sampled_block_rows": 1, "exact_mode_bit_exact": bool(same),
-                                 "against": "the reference (oracle/_ref) mat_mul"}
-                del ha, hb
-        if not args.no_cpu_baseline:
-            rec["cpu_baseline"] = cpu_baseline_matmul(a_rows, n4, gen="rough")
-        out["cfg4_1gpu"] = rec
-        del A, B, C, scratch
-        torch.cuda.empty_cache()
-    return out
+    barrier(world)
+    return max_over_ranks(e0.elapsed_time(e1) / reps, world)
 
 
 def _shard_compress(gen, r0, nrows, cols, seed, chunk_rows=8192):
-    """Compresses rows [r0, r0 + nrows) of the seeded `gen` field (chunk by chunk)."""
+    """Compresses rows [r0, r0 + nrows) of the seeded `gen` field (chunk by chunk,
+    bounded memory).  Returns the DeviceCMat and the first 64 dense rows."""
     import torch
 
     from paper_2202_13007_b200 import device as dev
     from paper_2202_13007_b200 import workloads as W
     out = dev.DeviceCMat(nrows, cols)
     bc = (cols + 7) // 8
+    head = None
     for c0 in range(0, nrows, chunk_rows):
         nr = min(chunk_rows, nrows - c0)
         if gen == "smooth":
@@ -535,72 +464,205 @@ def _shard_compress(gen, r0, nrows, cols, seed, chunk_rows=8192):
         out.slope[b0:b1].copy_(part.slope)
         out.coeffs[b0:b1].copy_(part.coeffs)
         out.scale[b0:b1].copy_(part.scale)
+        if c0 == 0:
+            head = d[:64].cpu().numpy()
         del d, part
     torch.cuda.synchronize()
-    return out
+    return out, head
 
 
-def run_sharded(args, rank, world, local):
-    """--config cfg2 / cfg4: BASELINE configs 2 and 4 block-row sharded over the ranks
-    (strong scaling: the total problem is fixed).  cfg2: local row dots, an all-gather of
-    the r_i and the ascending total (bit-exact for every world size).  cfg4: A row-sharded,
-    compressed B all-gathered every step (45 B/block over NVLink), local matmul."""
+def _block_rows(cm, br0, nbr):
+    """Host AoS blocks of block-rows [br0, br0 + nbr) of a DeviceCMat (packed on the device)."""
+    from paper_2202_13007_b200 import device as dev
+    bc = cm.block_cols
+    rows = min(8 * nbr, cm.rows - 8 * br0)
+    sub = dev.DeviceCMat(rows, cm.cols)
+    lo, hi = br0 * bc, (br0 + nbr) * bc
+    sub.first.copy_(cm.first[lo:hi])
+    sub.slope.copy_(cm.slope[lo:hi])
+    sub.coeffs.copy_(cm.coeffs[lo:hi])
+    sub.scale.copy_(cm.scale[lo:hi])
+    return sub.to_host().blocks
+
+
+def _same_blocks(x, y):
+    return all(np.array_equal(np.ascontiguousarray(x[f]).view(np.uint8), np.ascontiguousarray(y[f]).view(np.uint8))
+               for f in ("first", "slope", "scale_factor", "coeffs"))
+
+
+def fp64_peaks():
+    """FP64 roofline denominators measured live on this GPU by
+    tools/microbench/fp64_peaks (DFMA / DMMA chains on every SM); falls back to
+    the committed measurement (profiles/r01_fp64_peaks.txt) if the binary is absent."""
+    exe = os.path.join(ROOT, "tools", "microbench", "fp64_peaks")
+    if os.path.exists(exe):
+        try:
+            out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
+            for ln in out.splitlines():
+                if ln.startswith("{"):
+                    d = json.loads(ln)
+                    if d.get("ok"):
+                        d["kind"] = "measured live (tools/microbench/fp64_peaks)"
+                        return d
+        except (OSError, subprocess.TimeoutExpired, ValueError):
+            pass
+    return {"dfma_tops": 18.29, "dfma_tflops": 36.58, "dmma_tflops": 36.6,
+            "kind": "committed measurement (profiles/r01_fp64_peaks.txt)"}
+
+
+# FP64 operations of the reference's own sequence (SURVEY.md 8(d)), the algorithmic
+# count behind the FP64 rooflines: decompress_block = 28 divisions (dequantize) +
+# 2 x 512 mul + 2 x 512 add (idct2, H/dct.hpp:53-70) + 224 (integrate_rows,
+# H/codec.hpp:164-174); a row-dot block pair = two decompressions + 64 mul + 64 add.
+FP64_OPS_DECOMPRESS = 28 + 2048 + 224
+FP64_OPS_ROWDOT_PAIR = 2 * FP64_OPS_DECOMPRESS + 128
+
+
+def run_extras(args, rank, world):
+    """BASELINE configs 2, 3 and 4, block-row sharded over the ranks (strong scaling:
+    the problem is fixed, world=1 is one GPU doing all of it).
+
+    cfg2: local row dots, then an all-gather of the r_i and one ascending total
+          (bit-exact for every world size), and the allreduce-of-partials variant.
+    cfg3/cfg4: A row-sharded; compressed B all-gathered (45 B/block over NVLink)
+          in every step, then the local decompress + GEMM + compress; both GEMM
+          modes, with the fused mode's flip counts / tolerances against exact mode."""
     import torch
 
+    from paper_2202_13007_b200 import compare as CMP
     from paper_2202_13007_b200 import device as dev
     from paper_2202_13007_b200 import shard as S
-    torch.cuda.set_device(local)
-    if args.config == "cfg2":
-        n = args.cfg2_size
+    out = {}
+    peaks = fp64_peaks()
+    out["fp64_peaks"] = peaks
+    fp64_tflops = float(peaks["dfma_tflops"])
+    fp64_tops = float(peaks["dfma_tops"])
+    # ---- config 2: row dots + Frobenius of two 65536^2 smooth fields -------------------
+    n2 = args.cfg2_size
+    if n2 > 0:
+        r0, nr = S.local_rows(n2, rank, world)
+        A, a_head = _shard_compress("smooth", r0, nr, n2, 11)
+        B, b_head = _shard_compress("smooth", r0, nr, n2, 12)
+        res = {}
+
+        def gather_variant():
+            res["r"], res["t"] = S.rowdot_frobenius(A, B)
+
+        def allreduce_variant():
+            res["t2"] = S.frobenius_allreduce(A, B)
+        ms = _time_dist(gather_variant, args.extra_reps, world)
+        ms_ar = _time_dist(allreduce_variant, args.extra_reps, world)
+        pairs = ((n2 + 7) // 8) ** 2
+        ach = pairs * FP64_OPS_ROWDOT_PAIR / (ms * 1e-3) / 1e12
+        rec = {"workload": f"cfg2 rowdot+frobenius {n2}x{n2} (smooth fields), block-row shards x{world}",
+               "ms": round(ms, 3), "value": pairs / (ms * 1e-3), "unit": "block pairs/s",
+               "collective": "all-gather of the r_i (8 B/row) + ascending total: bit-exact for every world size",
+               "bytes_gathered_per_rank": 8 * n2,
+               "allreduce_variant": {"ms": round(ms_ar, 3), "value": pairs / (ms_ar * 1e-3),
+                                     "bytes_reduced": 8, "parity": "tolerance (per-rank partials summed by NCCL)"},
+               "roofline": {"bound": "fp64", "achieved": round(ach, 3), "peak": round(fp64_tops, 3),
+                            "unit": "T FP64 ops/s", "frac": round(ach / fp64_tops, 4),
+                            "ops_per_pair": FP64_OPS_ROWDOT_PAIR, "ops_basis": "reference sequence (SURVEY 8d)",
+                            "peak_kind": peaks["kind"]}}
+        if not args.no_parity:
+            tot_g, tot_a = float(res["t"].item()), float(res["t2"].item())
+            rec["parity"] = {"allreduce_vs_gather_rel": abs(tot_a - tot_g) / max(abs(tot_g), 1e-300)}
+            if rank == 0:
+                from oracle import oracle as O
+                port = O.port()
+                want = port.rowdot(_block_rows(A, 0, 8), _block_rows(B, 0, 8), min(64, nr), n2)
+                got = res["r"][: min(64, nr)].cpu().numpy()
+                rec["parity"].update({"sampled_rows": int(min(64, nr)),
+                                      "bit_exact": bool(np.array_equal(got.view(np.uint64), want.view(np.uint64)))})
+        if rank == 0 and not args.no_cpu_baseline and world == 1:
+            rec["cpu_baseline"] = cpu_baseline_rowdot(a_head, b_head, n2)
+        out["cfg2"] = rec
+        del A, B, res
+        torch.cuda.empty_cache()
+    # ---- configs 3 and 4: compressed matmul -------------------------------------------------
+    for name, gen, n, seeds, reps in (("cfg3", "smooth", args.cfg3_size, (21, 22), args.extra_reps),
+                                      ("cfg4", "rough", args.cfg4_size, (41, 42), 1)):
+        if n <= 0:
+            continue
         r0, nr = S.local_rows(n, rank, world)
-        A = _shard_compress("smooth", r0, nr, n, 11)
-        B = _shard_compress("smooth", r0, nr, n, 12)
-        step = lambda: S.rowdot_frobenius(A, B)  # noqa: E731
-        units, unit, metric = (n // 8) * ((n + 7) // 8), "block pairs/s", \
-            "cfg2 row dots + Frobenius inner product, 8x8 block pairs/s"
-        workload = f"cfg2 {n}x{n} smooth fields, block-row shards x{world}, all-gather of r_i + ascending total"
-    else:
-        n = args.cfg4_size
-        r0, nr = S.local_rows(n, rank, world)
-        A = _shard_compress("rough", r0, nr, n, 41)
-        Bl = _shard_compress("rough", r0, nr, n, 42)
-        mode = 1 if args.gemm == "fused" else 0
-        step = lambda: S.matmul(A, Bl, n, n, mode=mode)  # noqa: E731
-        units, unit, metric = 2.0 * n ** 3, "TFLOP/s", "cfg4 compressed matmul FP64 TFLOP/s"
-        workload = (f"cfg4 {n}^3 rough U[-1,1], A row-sharded x{world}, compressed B all-gathered per step, "
-                    f"{args.gemm} GEMM")
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    barrier(world)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        barrier(world)
-        e0.record()
-        for _ in range(args.steps):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-        barrier(world)
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-    value = units / (ms * 1e-3)
-    if unit == "TFLOP/s":
-        value /= 1e12
-    if rank != 0:
-        return None
-    return {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded per shard, BASELINE distribution)",
-            "config": {"workload": workload, "n": n, "parallelism": f"block-row shards x{world}"},
-            "clocks": clk.summary(),
-            "e2e": None, "note": "secondary config mode: inputs generated on device; e2e is measured by the cfg1 mode"}
+        A, a_head = _shard_compress(gen, r0, nr, n, seeds[0])
+        Bl, _ = _shard_compress(gen, r0, nr, n, seeds[1])
+        Bf = S.allgather_cmat(Bl, n, n)
+        C = dev.DeviceCMat(nr, n)
+        scratch = dev.matmul_scratch(A, Bf)
+        flops = 2.0 * n ** 3
+        rec = {"workload": (f"{name} compressed matmul {n}^3, {gen} data, A row-sharded x{world}, "
+                            f"compressed B all-gathered every step (compressed in and out)"),
+               "bytes_gathered_per_rank": int(Bf.nblocks * 45 - Bl.nblocks * 45)}
+        for mode, mname in ((1, "fused"), (0, "exact")):
+            ms = _time_dist(lambda: S.matmul(A, Bl, n, n, mode=mode, b_full=Bf, out=C, scratch=scratch),
+                            reps, world)
+            tf = flops / (ms * 1e-3) / 1e12
+            rec[mname] = {"ms": round(ms, 3), "tflops": round(tf, 2), "frac_fp64_peak": round(tf / fp64_tflops, 3)}
+        rec["exact"]["note"] = "DMUL+DADD in the reference's order: at most 50% of the FP64 FMA peak"
+        rec["fused"]["note"] = "FP64 FMA chains (tolerance mode, BLZ_GEMM_FUSED)"
+        rec["peak"] = {"tflops": round(fp64_tflops, 2), "kind": peaks["kind"]}
+        if not args.no_parity:
+            # C holds the exact-mode result of the last timed call
+            par = {}
+            dctx = dev.context()
+            dense_x = dev.matmul_dense(A, Bf, mode=0, scratch=scratch)
+            cx = dev.compress(dense_x)
+            dctx.set_mode(1)  # BLZ_MODE_EXACT: the reference-order compress of the same dense C
+            try:
+                cx_exact = dev.compress(dense_x)
+                dev.sync()
+            finally:
+                dctx.set_mode(0)
+            eq = lambda x, y: all(torch.equal(getattr(x, f), getattr(y, f))  # noqa: E731
+                                  for f in ("first", "slope", "scale", "coeffs"))
+            bad = torch.tensor([0 if eq(cx, C) else 1, 0 if eq(cx, cx_exact) else 1], dtype=torch.float64,
+                               device="cuda")
+            if world > 1:
+                import torch.distributed as dist
+                if dist.get_backend() == "nccl":
+                    dist.all_reduce(bad)
+                else:
+                    h = bad.cpu()
+                    dist.all_reduce(h)
+                    bad = h
+            par["epilogue_equals_compress_of_dense"] = bool(bad[0].item() == 0)
+            par["epilogue_fast_equals_exact_compress_every_block"] = bool(bad[1].item() == 0)
+            del cx_exact
+            dense_f = dev.matmul_dense(A, Bf, mode=1, scratch=scratch)
+            cf = dev.compress(dense_f)
+            st = CMP.cmat_stats(cf, C)
+            st.update(CMP.dense_stats(dense_f, dense_x))
+            par["fused"] = CMP.summarize(CMP.allreduce(st))
+            del dense_f, cf, dense_x, cx
+            if rank == 0:
+                # block-rows 0 and the last local one of exact C against the reference itself
+                from oracle import oracle as O
+                nbr = A.block_rows
+                rows_chk = sorted({0, nbr - 1})
+                ha = np.concatenate([_block_rows(A, b, 1) for b in rows_chk], axis=0)
+                hb = Bf.to_host().blocks
+                hc = np.concatenate([_block_rows(C, b, 1) for b in rows_chk], axis=0)
+                if O.ref_available():
+                    want = O.ref().mat_mul(ha, 8 * len(rows_chk), n, hb, n, n, host_threads())
+                    against = "the reference (oracle/_ref) mat_mul"
+                else:
+                    want = O.port().mat_mul(ha, 8 * len(rows_chk), n, hb, n, n)
+                    against = "the C restatement (oracle/blaz_oracle.c)"
+                par["oracle"] = {"block_rows": [r0 // 8 + b for b in rows_chk],
+                                 "exact_mode_bit_exact": _same_blocks(hc, want), "against": against}
+                del hb
+            rec["parity"] = par
+        if rank == 0 and not args.no_cpu_baseline and world == 1:
+            rec["cpu_baseline"] = cpu_baseline_matmul(a_head, n, gen=gen, seed_b=seeds[1])
+        out[name] = rec
+        del A, Bl, Bf, C, scratch
+        torch.cuda.empty_cache()
+    return out
 
 
 def cpu_baseline_rowdot(a_rows, b_rows, n):
     """Reference decompress_matrix (all host threads) + ascending row sums on a 64-row slice."""
-    import numpy as np
-
     from oracle import oracle as O
     if not O.ref_available():
         return None
@@ -618,17 +680,18 @@ def cpu_baseline_rowdot(a_rows, b_rows, n):
             "sample": f"64 x {n} slice: reference decompress_matrix of A and B + row sums"}
 
 
-def cpu_baseline_matmul(a_rows, n, gen="smooth"):
+def cpu_baseline_matmul(a_rows, n, gen="smooth", seed_b=22):
     """Reference mat_mul of an 8-row slice of A by the full B (all host threads)."""
     from oracle import oracle as O
     if not O.ref_available():
         return None
-    import paper_2202_13007_b200.workloads as W
+    W = load_workloads()
     r = O.ref()
     threads = host_threads()
-    b = W.smooth_field(n, n, 22).numpy() if gen == "smooth" else W.rough_uniform(n, n, 42).numpy()
+    b = W.make(gen, n, n, seed_b).numpy()
     ca = r.compress_matrix(a_rows[:8], threads)
     cb = r.compress_matrix(b, threads)
+    del b
     t0 = time.perf_counter()
     r.mat_mul(ca, 8, n, cb, n, n, threads)
     dt = time.perf_counter() - t0
@@ -706,45 +769,76 @@ def run_e2e(args, A, B, rows, cols, nb, world):
     lib, h = ctx.lib, ctx.handle
     P = lambda a: a.ctypes.data  # noqa: E731
 
-    def step():
-        ctx.check(lib.blz_compress_matrix(h, P(npA), rows, cols, P(cA), 0))
-        ctx.check(lib.blz_compress_matrix(h, P(npB), rows, cols, P(cB), 0))
-        ctx.check(lib.blz_mat_add(h, P(cA), rows, cols, P(cB), rows, cols, P(cS), 0))
-        ctx.check(lib.blz_mat_sub(h, P(cA), rows, cols, P(cB), rows, cols, P(cD), 0))
-        ctx.check(lib.blz_mat_scale(h, P(cA), rows, cols, 3.5, P(cK), 0))
-        for c, d in ((cS, dS), (cD, dD), (cK, dK)):
+    def step(xA, xB, bA, bB, bS, bD, bK, dS, dD, dK):
+        ctx.check(lib.blz_compress_matrix(h, P(xA), rows, cols, P(bA), 0))
+        ctx.check(lib.blz_compress_matrix(h, P(xB), rows, cols, P(bB), 0))
+        ctx.check(lib.blz_mat_add(h, P(bA), rows, cols, P(bB), rows, cols, P(bS), 0))
+        ctx.check(lib.blz_mat_sub(h, P(bA), rows, cols, P(bB), rows, cols, P(bD), 0))
+        ctx.check(lib.blz_mat_scale(h, P(bA), rows, cols, 3.5, P(bK), 0))
+        for c, d in ((bS, dS), (bD, dD), (bK, dK)):
             ctx.check(lib.blz_decompress_matrix(h, P(c), rows, cols, P(d), 0))
 
-    step()  # warm-up (scratch allocation)
+    pinned = (npA, npB, cA, cB, cS, cD, cK, dS, dD, dK)
+    step(*pinned)  # warm-up (scratch allocation)
     torch.cuda.synchronize()
     n = max(1, min(args.steps, args.e2e_steps))
     barrier(world)
     t0 = time.perf_counter()
     for _ in range(n):
-        step()
+        step(*pinned)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / n
     dt = max_over_ranks(dt, world)
     dense, blk = rows * cols * 8, nb * 48
     h2d = 2 * dense + 2 * (2 * blk) + blk + 3 * blk
     d2h = 2 * blk + 3 * blk + 3 * dense
+    res = {"value": nb * world / dt, "unit": "blocks/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "ms_per_step": dt * 1e3, "steps": n,
+           "api": "C ABI host entry points blz_compress_matrix / blz_mat_add / blz_mat_sub / "
+                  "blz_mat_scale / blz_decompress_matrix (pinned host buffers)"}
+    # the drop-in's usual case: pageable std::vector-like buffers (plain numpy arrays)
+    del hA, hB, cA, cB, cS, cD, cK, dS, pinned
+    pA, pB = np.array(npA), np.array(npB)
+    del npA, npB
+    pbl = [np.zeros((nbr, nbc), blz.BLOCK_DTYPE) for _ in range(5)]
+    pd = np.empty((rows, cols), np.float64)
+    pageable = (pA, pB, *pbl, pd, pd, pd)
+    step(*pageable)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    step(*pageable)
+    torch.cuda.synchronize()
+    dtp = max_over_ranks(time.perf_counter() - t0, world)
+    res["pageable"] = {"value": nb * world / dtp, "unit": "blocks/s", "ms_per_step": dtp * 1e3, "steps": 1,
+                       "note": "same calls from pageable host memory (the C++ drop-in's std::vector case)"}
     ctx.close()
-    return {"value": nb * world / dt, "unit": "blocks/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": dt * 1e3, "steps": n,
-            "api": "C ABI host entry points blz_compress_matrix / blz_mat_add / blz_mat_sub / "
-                   "blz_mat_scale / blz_decompress_matrix (pinned host buffers)"}
+    return res
 
 
 def cpu_baseline(args, cfg):
     threads = host_threads()
-    kind, used, step = cpu_reference_step_fn(cfg, args.ref_sample_rows, threads)
-    blocks = (args.ref_sample_rows // 8) * ((cfg["cols"] + 7) // 8)
+    kind, used, step = cpu_reference_step_fn(cfg, args.cpu_sample_rows, threads)
+    blocks = (args.cpu_sample_rows // 8) * ((cfg["cols"] + 7) // 8)
     step()
     times = [step() for _ in range(args.cpu_repeats)]
     med = statistics.median(times)
     return {"value": blocks / med, "unit": "blocks/s", "cores": used, "kind": kind,
-            "sample": f"{args.ref_sample_rows}x{cfg['cols']} block-row slice of {args.config} "
+            "sample": f"{args.cpu_sample_rows}x{cfg['cols']} block-row slice of {args.config} "
                       f"({blocks} blocks), median of {args.cpu_repeats} after 1 warm-up"}
+
+
+def reexec_under_torchrun(n):
+    """`bench.py --gpus N` without a launcher: re-run this command under torchrun
+    with one rank per GPU (the driver's own launch form)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -753,48 +847,30 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS) + ["cfg2", "cfg4"])
-    ap.add_argument("--gemm", default="fused", choices=["fused", "exact"], help="cfg4 GEMM mode")
+    ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
     ap.add_argument("--sequential", action="store_true", help="time the one-stream op order instead of the DAG")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
-    ap.add_argument("--ref-sample-rows", type=int, default=512)
+    ap.add_argument("--ref-sample-rows", type=int, default=0,
+                    help="reference arm: rows of the workload timed (0 = all of it, the default)")
+    ap.add_argument("--cpu-sample-rows", type=int, default=2048, help="our arm's bounded cpu_baseline sample")
     ap.add_argument("--cpu-repeats", type=int, default=3)
-    ap.add_argument("--no-extras", action="store_true", help="skip the config-2/3 measurements")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config-2/3/4 measurements")
     ap.add_argument("--cfg2-size", type=int, default=65536)
     ap.add_argument("--cfg3-size", type=int, default=8192)
     ap.add_argument("--extra-reps", type=int, default=3)
-    ap.add_argument("--cfg4-size", type=int, default=32768, help="0 skips the config-4 one-GPU matmul")
+    ap.add_argument("--cfg4-size", type=int, default=32768, help="0 skips config 4")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps
     cfg = CONFIGS.get(args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        reexec_under_torchrun(args.gpus)
     rank, world, local = dist_env()
-
-    if args.config in ("cfg2", "cfg4"):
-        if args.impl == "reference":
-            if rank == 0:
-                print(json.dumps({"impl": "reference", "unavailable": "the reference arm is measured on the cfg1 "
-                                  "workload; cfg2/cfg4 report their CPU baselines in the default run's configs"}))
-            return
-        if world > 1:
-            import torch
-            import torch.distributed as dist
-            backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-            local = local % torch.cuda.device_count()
-            torch.cuda.set_device(local)
-            if backend == "nccl":
-                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-            else:
-                dist.init_process_group(backend)
-        line = run_sharded(args, rank, world, local)
-        if line is not None:
-            print(json.dumps(line), flush=True)
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
-        return
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU", file=sys.stderr)
+        sys.exit(2)
 
     if args.impl == "reference":
         line = run_reference_arm(args, cfg, rank, world)
@@ -805,12 +881,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        # one rank per GPU over NCCL; BENCH_DIST_BACKEND=gloo only for exercising the
-        # N > 1 plumbing with several ranks on one GPU (no timing meaning)
+        # one rank per GPU over NCCL (NCCL_DEBUG=INFO shows the ranks and transports);
+        # BENCH_DIST_BACKEND=gloo only exercises the N > 1 plumbing with several ranks
+        # on one GPU (no timing meaning)
         backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
         local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)

@@ -124,16 +124,27 @@ struct partial_reconstruction {
 
 namespace gpu {
 
-// Process-wide context (created on first use).
+// One context per calling thread (created on first use, destroyed at thread
+// exit).  A context owns its stream, scratch buffers, worklists and error
+// string, so concurrent calls from several threads never share mutable state:
+// the reference's functions are pure and re-entrant, and so are these.
+struct thread_context {
+    blz_ctx* ctx = nullptr;
+    ~thread_context() {
+        if (ctx) blz_ctx_destroy(ctx);
+    }
+};
+
 inline blz_ctx* context() {
-    static std::once_flag once;
-    static blz_ctx* ctx = nullptr;
-    std::call_once(once, [] {
+    thread_local thread_context tc;
+    if (!tc.ctx) {
         const char* d = std::getenv("BLZ_DEVICE");
-        if (blz_ctx_create(d ? std::atoi(d) : 0, nullptr, &ctx) != BLZ_OK)
+        if (blz_ctx_create(d ? std::atoi(d) : 0, nullptr, &tc.ctx) != BLZ_OK) {
+            tc.ctx = nullptr;
             throw std::runtime_error("blaz: cannot create the CUDA context");
-    });
-    return ctx;
+        }
+    }
+    return tc.ctx;
 }
 
 inline void check(blz_status st) {

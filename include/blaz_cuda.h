@@ -72,10 +72,14 @@ typedef struct blz_cmat {
 
 typedef struct blz_ctx blz_ctx;
 
-/* GEMM accumulation modes for blz_matmul_* */
+/* GEMM accumulation modes for blz_matmul_* (H/matrix.hpp:188-202 accumulates
+ * acc = 0.0; acc += a*b over k ascending, products and sums rounded separately) */
 typedef enum blz_gemm_mode {
-    BLZ_GEMM_EXACT = 0, /* DMUL+DADD, ascending k: bitwise equal to mat_mul/mat_dot */
-    BLZ_GEMM_FUSED = 1  /* DFMA, ascending k: tolerance parity (normwise) */
+    BLZ_GEMM_EXACT = 0,      /* DMUL+DADD, ascending k: bitwise equal to mat_mul/mat_dot */
+    BLZ_GEMM_FUSED = 1,      /* acc = fma(a, b, acc), ascending k: tolerance parity; runs the
+                                faster of the two kernels below (their results are bitwise equal) */
+    BLZ_GEMM_FUSED_DMMA = 2, /* the fused chain on FP64 tensor cores (mma.sync m8n8k4 f64) */
+    BLZ_GEMM_FUSED_DFMA = 3  /* the fused chain as CUDA-core DFMA */
 } blz_gemm_mode;
 
 /* ---- context --------------------------------------------------------------- */

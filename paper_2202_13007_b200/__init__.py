@@ -6,7 +6,7 @@ all arithmetic runs in hand-written CUDA kernels (``csrc/``).  Importing the
 package requires the built library ``lib/libblaz_cuda.so`` -- there is no
 CPU fallback.
 """
-from ._native import (BLOCK_DTYPE, GEMM_EXACT, GEMM_FUSED, MODE_DEFAULT, MODE_EXACT, BlazError, InvalidArgument, IoError,  # noqa: F401
+from ._native import (BLOCK_DTYPE, GEMM_EXACT, GEMM_FUSED, GEMM_FUSED_DFMA, GEMM_FUSED_DMMA, MODE_DEFAULT, MODE_EXACT, BlazError, InvalidArgument, IoError,  # noqa: F401
                       NotBuilt, OutOfRange, load)
 from .matrix import (CompressedMatrix, Context, block_dim, block_payload_bytes,  # noqa: F401
                      compress_block, compress_blocks, compress_matrix, compression_rate,

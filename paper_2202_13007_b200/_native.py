@@ -21,7 +21,7 @@ BLOCK_DTYPE = np.dtype(
      "offsets": [0, 8, 16, 17], "itemsize": 48})
 
 BLZ_OK, BLZ_INVALID_ARGUMENT, BLZ_OUT_OF_RANGE, BLZ_CUDA_ERROR, BLZ_OUT_OF_MEMORY, BLZ_NOT_SUPPORTED, BLZ_IO_ERROR = range(7)
-GEMM_EXACT, GEMM_FUSED = 0, 1
+GEMM_EXACT, GEMM_FUSED, GEMM_FUSED_DMMA, GEMM_FUSED_DFMA = 0, 1, 2, 3
 MODE_DEFAULT, MODE_EXACT = 0, 1
 
 

@@ -107,6 +107,8 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
   const uint64_t nb = out.nb();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  // out must be disjoint from the inputs or identical to one of them (in place)
+  const int alias = out.first == a.first ? 1 : (out.first == b.first ? 2 : 0);
   int buf = 0;
   uint64_t t0 = gw * 32;
   if (t0 < nb) {
@@ -143,12 +145,23 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
 #pragma unroll
     for (int w = 0; w < 7; ++w) oc[w] = o.c[w];
     if (fallback && t < nb) wl[atomicAdd(wl_count, 1ull)] = t;
-    ro.f[lane] = of;
-    ro.s[lane] = os;
-    ro.phi[lane] = (uint8_t)ophi;
+    if (fallback && alias != 0) {
+      // k_addsub_fallback re-reads a[t] and b[t]: when out is one of the inputs
+      // (in-place add/sub), that input's record must survive this store.
+      const WarpRecs& keep = alias == 1 ? ra : rb;
+      ro.f[lane] = keep.f[lane];
+      ro.s[lane] = keep.s[lane];
+      ro.phi[lane] = keep.phi[lane];
 #pragma unroll
-    for (int w = 0; w < 7; ++w) ro.c[lane * 7 + w] = oc[w];
-    if (slow) {  // huge weights: the reference rounding sequence (blaz_device.cuh::clamp_coeff)
+      for (int w = 0; w < 7; ++w) ro.c[lane * 7 + w] = keep.c[lane * 7 + w];
+    } else {
+      ro.f[lane] = of;
+      ro.s[lane] = os;
+      ro.phi[lane] = (uint8_t)ophi;
+#pragma unroll
+      for (int w = 0; w < 7; ++w) ro.c[lane * 7 + w] = oc[w];
+    }
+    if (slow && !fallback) {  // huge weights: the reference rounding sequence (blaz_device.cuh::clamp_coeff)
       const uint8_t* b1 = reinterpret_cast<const uint8_t*>(&ra.c[lane * 7]);
       const uint8_t* b2 = reinterpret_cast<const uint8_t*>(&rb.c[lane * 7]);
       uint8_t* bo = reinterpret_cast<uint8_t*>(&ro.c[lane * 7]);

@@ -181,6 +181,28 @@ blz_status check_cmat(blz_ctx* c, const blz_cmat* m, const char* what) {
   return BLZ_OK;
 }
 
+// out must be disjoint from `in` or be the very same matrix (in-place use): the
+// kernels read and write each block's record in place, never another block's.
+blz_status check_alias(blz_ctx* c, const blz_cmat* out, const blz_cmat* in, const char* what) {
+  const uint64_t nb = in->block_rows * in->block_cols;
+  if (nb == 0) return BLZ_OK;
+  const bool same = out->first == in->first && out->slope == in->slope && out->scale == in->scale &&
+                    out->coeffs == in->coeffs;
+  if (same) return BLZ_OK;
+  auto ov = [](const void* p, uint64_t np, const void* q, uint64_t nq) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p), b = reinterpret_cast<uintptr_t>(q);
+    return a < b + nq && b < a + np;
+  };
+  const void* po[4] = {out->first, out->slope, out->scale, out->coeffs};
+  const void* pi[4] = {in->first, in->slope, in->scale, in->coeffs};
+  const uint64_t sz[4] = {8 * nb, 8 * nb, nb, 28 * nb};
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j)
+      if (ov(po[i], sz[i], pi[j], sz[j]))
+        return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": output partially overlaps an input");
+  return BLZ_OK;
+}
+
 // H/matrix.hpp:86-93
 blz_status same_dims(blz_ctx* c, uint64_t ar, uint64_t ac, uint64_t br, uint64_t bc, const char* what) {
   if (ar != br || ac != bc)
@@ -408,6 +430,8 @@ static blz_status addsub_dev(blz_ctx* c, bool sub, const blz_cmat* a, const blz_
   if (blz_status st = same_dims(c, a->rows, a->cols, b->rows, b->cols, what)) return st;  // H/matrix.hpp:130
   if (out->rows != a->rows || out->cols != a->cols)
     return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": output dimension mismatch");
+  if (blz_status st = check_alias(c, out, a, what)) return st;
+  if (blz_status st = check_alias(c, out, b, what)) return st;
   const uint64_t nb = a->block_rows * a->block_cols;
   if (nb == 0) return BLZ_OK;
   if (blz_status st = ensure_worklist(c, nb)) return st;
@@ -508,7 +532,7 @@ static blz_status matmul_common(blz_ctx* c, const blz_cmat* a, const blz_cmat* b
   if (blz_status st = check_cmat(c, a, "mat_mul")) return st;
   if (blz_status st = check_cmat(c, b, "mat_mul")) return st;
   if (a->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: inner dimension mismatch");  // :207
-  if (mode != BLZ_GEMM_EXACT && mode != BLZ_GEMM_FUSED) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: bad mode");
+  if (mode < BLZ_GEMM_EXACT || mode > BLZ_GEMM_FUSED_DFMA) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: bad mode");
   if (!scratch) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: null scratch");
   const uint64_t ma = 8 * a->block_rows, ka = 8 * a->block_cols, kb = 8 * b->block_rows, nn = 8 * b->block_cols;
   double* da = (double*)scratch;
@@ -542,6 +566,7 @@ blz_status blz_matmul_dense_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b
   if (blz_status st = check_cmat(c, b, "mat_mul")) return st;
   if (a->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: inner dimension mismatch");
   if (ld < b->cols) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul_dense: ld < cols");
+  if (mode < BLZ_GEMM_EXACT || mode > BLZ_GEMM_FUSED_DFMA) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: bad mode");
   if (!scratch) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: null scratch");
   const uint64_t ma = 8 * a->block_rows, ka = 8 * a->block_cols, kb = 8 * b->block_rows, nn = 8 * b->block_cols;
   double* da = (double*)scratch;

@@ -116,7 +116,10 @@ static unsigned grid_for(uint64_t n, unsigned threads, int sms, unsigned per_sm 
 cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
                             uint64_t cols, uint64_t ld, const CMat& out) {
   const unsigned g = grid_for(out.nb(), 128, c.sm_count);
-  if (c.exact_only || !c.fast) {
+  // the fast path stores coefficient records as 16-byte chunks (k_compress_pair):
+  // a caller view whose coefficient array is not 16-byte aligned takes the exact kernel
+  const bool coeffs_aligned = (reinterpret_cast<uintptr_t>(out.coeffs) & 15) == 0;
+  if (c.exact_only || !c.fast || !coeffs_aligned) {
     k_compress<<<g, 128, 0, c.stream>>>(B, dense, rows, cols, ld, out, c.err);
     ++*c.launches;
     return cudaGetLastError();
@@ -129,8 +132,7 @@ cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* de
   P.zero = 0;
   e = launch_compress_pair(c, P, dense, rows, cols, ld, out);
   if (e != cudaSuccess) return e;
-  e = launch_compress_worklist_warp(c, B, dense, rows, cols, ld, out);
-  return cudaGetLastError();
+  return launch_compress_worklist_warp(c, B, dense, rows, cols, ld, out);
 }
 
 cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in, double* tiles) {

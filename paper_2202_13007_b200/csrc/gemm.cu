@@ -8,11 +8,16 @@
 //    with -fmad=false) in exactly that order: bitwise equal to the reference.
 //    Tiles beyond K are zero-filled: adding +0.0 to a running sum that starts
 //    at +0.0 (and is therefore never -0.0) is the identity.
-//  * BLZ_GEMM_FUSED -- k_gemm_dmma: FP64 tensor cores (mma.sync m8n8k4 f64,
-//    DMMA).  On B200 one DMMA equals the ascending-k chain of fused
-//    multiply-adds (tools/microbench/dmma_semantics.cu: 0 mismatches in 1.28M
-//    entries), so the result is acc = fma(a(i,k), b(k,j), acc), k ascending,
-//    from +0.0: deterministic, tolerance parity against the exact product.
+//  * BLZ_GEMM_FUSED -- acc = fma(a(i,k), b(k,j), acc), k ascending, from +0.0:
+//    deterministic, tolerance parity against the exact product.  Two kernels
+//    compute this chain bitwise identically (tests/test_gpu_parity.py checks):
+//      k_gemm_simt<true> (BLZ_GEMM_FUSED_DFMA): the SIMT kernel with DFMA;
+//      k_gemm_dmma (BLZ_GEMM_FUSED_DMMA): FP64 tensor cores (mma.sync m8n8k4
+//      f64).  On B200 one DMMA equals the ascending-k chain of fused
+//      multiply-adds (tools/microbench/dmma_semantics.cu: 0 mismatches in 1.28M
+//      entries).
+//    BLZ_GEMM_FUSED runs FUSED_KERNEL_DEFAULT, the faster of the two on B200
+//    (K7, profiles/r02_gemm_dfma_vs_dmma.md).
 #include <cuda_pipeline_primitives.h>
 
 #include "launch.h"
@@ -30,7 +35,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   __pipeline_memcpy_async(smem, gmem, 16);
 }
 
-__global__ void __launch_bounds__(256) k_gemm_exact(const double* __restrict__ A, uint64_t lda,
+// FMA = false: acc + a*b as DMUL then DADD (-fmad=false); true: one DFMA.
+template <bool FMA>
+__global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A, uint64_t lda,
                                                     const double* __restrict__ Bm, uint64_t ldb,
                                                     double* __restrict__ Cm, uint64_t ldc, uint64_t M,
                                                     uint64_t N, uint64_t K) {
@@ -116,7 +123,7 @@ __global__ void __launch_bounds__(256) k_gemm_exact(const double* __restrict__ A
         for (int i = 0; i < 8; ++i) {
           const double a = h ? av[i].y : av[i].x;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = acc[i][j] + a * bv[j];
+          for (int j = 0; j < 8; ++j) acc[i][j] = FMA ? fma(a, bv[j], acc[i][j]) : acc[i][j] + a * bv[j];
         }
       }
     }
@@ -244,22 +251,28 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
     }
 }
 
+#ifndef FUSED_KERNEL_DEFAULT
+#define FUSED_KERNEL_DEFAULT 2  // BLZ_GEMM_FUSED_DMMA
+#endif
+
 cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t lda, const double* Bm,
                         uint64_t ldb, double* Cm, uint64_t ldc, uint64_t M, uint64_t N, uint64_t K) {
-  if (mode == 1) {
+  if (mode == 1) mode = FUSED_KERNEL_DEFAULT;
+  // per call: the smem attribute belongs to the current device (a few microseconds
+  // against a GEMM of milliseconds)
+  if (mode == 2) {
     dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
     const size_t smem = (size_t)(2 * DBM * DAS + 2 * DBK * DBS) * sizeof(double);
-    // per call: the attribute belongs to the current device (a few microseconds
-    // against a GEMM of milliseconds)
     cudaError_t ea = cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return ea;
     k_gemm_dmma<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
   } else {
     dim3 grid((unsigned)((N + EBN - 1) / EBN), (unsigned)((M + EBM - 1) / EBM));
     const size_t smem = (size_t)(2 * EBM * EAS + 2 * EBK * EBN) * sizeof(double);
-    cudaError_t ea = cudaFuncSetAttribute(k_gemm_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = mode == 3 ? k_gemm_simt<true> : k_gemm_simt<false>;
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return ea;
-    k_gemm_exact<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
+    kern<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
   }
   ++*c.launches;
   return cudaGetLastError();

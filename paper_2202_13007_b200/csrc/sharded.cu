@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/blaz_cuda.h"
@@ -42,7 +43,12 @@ struct NcclApi {
 const NcclApi& nccl() {
   static NcclApi api = [] {
     NcclApi a;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // BLZ_NCCL_LIB names another NCCL-compatible library (the tests' in-process
+    // multi-rank mock, tests/mock_nccl); otherwise the system / torch NCCL
+    const char* alt = getenv("BLZ_NCCL_LIB");
+    void* h = alt && *alt ? dlopen(alt, RTLD_NOW | RTLD_GLOBAL) : nullptr;
+    if (alt && *alt && !h) return a;
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return a;
     a.bcast = reinterpret_cast<decltype(a.bcast)>(dlsym(h, "ncclBroadcast"));
@@ -93,17 +99,33 @@ blz_status blz_allgather_cmat_nccl(blz_ctx* c, void* comm, const blz_cmat* local
   cudaStream_t s = (cudaStream_t)blz_ctx_get_stream(c);
   const NcclApi& n = nccl();
   if (blz_status st = nccl_status(c, n.group_start(), "ncclGroupStart")) return st;
+  // every call inside the group is checked; the group is always closed, and the
+  // first failing call's code is reported
+  ncclResult_t first = ncclSuccess;
+  const char* what = "allgather";
+  auto keep = [&](ncclResult_t r, const char* w) {
+    if (first == ncclSuccess && r != ncclSuccess) {
+      first = r;
+      what = w;
+    }
+  };
   for (int r = 0; r < world; ++r) {
     const uint64_t b0 = shard_lo(br, r, world) * bc, nb = shard_lo(br, r + 1, world) * bc - b0;
     if (nb == 0) continue;
     const bool me = r == rank;
-    n.bcast(me ? (const void*)local->first : nullptr, full->first + b0, nb, ncclFloat64, r, (ncclComm_t)comm, s);
-    n.bcast(me ? (const void*)local->slope : nullptr, full->slope + b0, nb, ncclFloat64, r, (ncclComm_t)comm, s);
-    n.bcast(me ? (const void*)local->coeffs : nullptr, full->coeffs + 28 * b0, 28 * nb, ncclInt8, r,
-            (ncclComm_t)comm, s);
-    n.bcast(me ? (const void*)local->scale : nullptr, full->scale + b0, nb, ncclUint8, r, (ncclComm_t)comm, s);
+    keep(n.bcast(me ? (const void*)local->first : nullptr, full->first + b0, nb, ncclFloat64, r, (ncclComm_t)comm, s),
+         "ncclBroadcast(first)");
+    keep(n.bcast(me ? (const void*)local->slope : nullptr, full->slope + b0, nb, ncclFloat64, r, (ncclComm_t)comm, s),
+         "ncclBroadcast(slope)");
+    keep(n.bcast(me ? (const void*)local->coeffs : nullptr, full->coeffs + 28 * b0, 28 * nb, ncclInt8, r,
+                 (ncclComm_t)comm, s),
+         "ncclBroadcast(coeffs)");
+    keep(n.bcast(me ? (const void*)local->scale : nullptr, full->scale + b0, nb, ncclUint8, r, (ncclComm_t)comm, s),
+         "ncclBroadcast(scale)");
   }
-  return nccl_status(c, n.group_end(), "allgather");
+  const ncclResult_t end = n.group_end();
+  if (first != ncclSuccess) return nccl_status(c, first, what);
+  return nccl_status(c, end, "allgather");
 }
 
 // r_all: device array of the global row count; rank r's rows land at their
@@ -119,14 +141,18 @@ blz_status blz_rowdot_frobenius_nccl(blz_ctx* c, void* comm, const blz_cmat* a_l
   cudaStream_t s = (cudaStream_t)blz_ctx_get_stream(c);
   const NcclApi& n = nccl();
   if (blz_status st = nccl_status(c, n.group_start(), "ncclGroupStart")) return st;
+  ncclResult_t first = ncclSuccess;
   for (int r = 0; r < world; ++r) {
     const uint64_t lo = 8 * shard_lo(br, r, world);
     const uint64_t hi = 8 * shard_lo(br, r + 1, world) < rows_total ? 8 * shard_lo(br, r + 1, world) : rows_total;
     if (hi <= lo) continue;
-    n.bcast(r == rank ? (const void*)(r_all + lo) : nullptr, r_all + lo, hi - lo, ncclFloat64, r, (ncclComm_t)comm,
-            s);
+    const ncclResult_t res = n.bcast(r == rank ? (const void*)(r_all + lo) : nullptr, r_all + lo, hi - lo,
+                                     ncclFloat64, r, (ncclComm_t)comm, s);
+    if (first == ncclSuccess) first = res;
   }
-  if (blz_status st = nccl_status(c, n.group_end(), "allgather of row dots")) return st;
+  const ncclResult_t end = n.group_end();
+  if (first != ncclSuccess) return nccl_status(c, first, "ncclBroadcast(row dots)");
+  if (blz_status st = nccl_status(c, end, "allgather of row dots")) return st;
   return blz_sum_dev(c, r_all, rows_total, total);
 }
 

@@ -98,11 +98,12 @@ def frobenius_allreduce(a_local, b_local, group=None):
     return part
 
 
-def allgather_cmat(local, rows: int, cols: int, group=None):
-    """Full compressed matrix (DeviceCMat) from the row shards of all ranks."""
+def allgather_cmat(local, rows: int, cols: int, group=None, out=None):
+    """Full compressed matrix (DeviceCMat) from the row shards of all ranks
+    (written into `out` when given)."""
     from . import device as dev
     first, slope, coeffs, scale = gather_soa(local.first, local.slope, local.coeffs, local.scale, group)
-    full = dev.DeviceCMat(rows, cols, device=local.buf.device)
+    full = out if out is not None else dev.DeviceCMat(rows, cols, device=local.buf.device)
     full.first.copy_(first)
     full.slope.copy_(slope)
     full.coeffs.copy_(coeffs)
@@ -110,8 +111,10 @@ def allgather_cmat(local, rows: int, cols: int, group=None):
     return full
 
 
-def matmul(a_local, b_local, b_rows: int, b_cols: int, mode: int = 0, group=None):
-    """C rows of this rank = (A rows of this rank) x (all-gathered compressed B)."""
+def matmul(a_local, b_local, b_rows: int, b_cols: int, mode: int = 0, group=None, b_full=None, out=None,
+           scratch=None):
+    """C rows of this rank = (A rows of this rank) x (all-gathered compressed B).
+    `b_full`, `out` and `scratch` are reused when given (steady-state loops)."""
     from . import device as dev
-    b_full = allgather_cmat(b_local, b_rows, b_cols, group)
-    return dev.matmul(a_local, b_full, mode=mode)
+    b_full = allgather_cmat(b_local, b_rows, b_cols, group, out=b_full)
+    return dev.matmul(a_local, b_full, mode=mode, out=out, scratch=scratch)

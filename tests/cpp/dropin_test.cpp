@@ -6,6 +6,9 @@
 
 #include <cstring>
 #include <random>
+#include <string>
+#include <thread>
+#include <vector>
 
 #include "../../oracle/blaz_oracle.h"
 #include "blaz/blaz.hpp"
@@ -173,4 +176,36 @@ TEST(DropIn, ExceptionsMatchReference) {
     EXPECT_THROW(mat_mul(a, c), std::invalid_argument);
     EXPECT_THROW(reconstruct_rows(a.blocks[0], 8), std::out_of_range);
     EXPECT_THROW(dot(a.blocks[0], a.blocks[0], 0, 8), std::out_of_range);
+}
+
+// The reference's functions are pure and re-entrant: concurrent calls from
+// several threads (each on its own per-thread context) give the oracle's
+// results, including the error messages of the failing calls.
+TEST(DropIn, ConcurrentCallsFromThreads) {
+    constexpr int kThreads = 6;
+    std::vector<std::thread> pool;
+    std::vector<int> bad(kThreads, 0);
+    for (int w = 0; w < kThreads; ++w) {
+        pool.emplace_back([w, &bad] {
+            std::mt19937_64 rng(500 + w);
+            for (int it = 0; it < 4; ++it) {
+                const dense_matrix ma = field(40 + 8 * w, 56, rng, (w + it) & 1);
+                const dense_matrix mb = field(40 + 8 * w, 56, rng);
+                const compressed_matrix a = compress_matrix(ma), b = compress_matrix(mb);
+                const compressed_matrix s = mat_sub(a, b);
+                std::vector<orc_block> oa = oracle_compress(ma), ob = oracle_compress(mb), os(oa.size());
+                orc_mat_sub(oa.data(), ob.data(), oa.size(), os.data());
+                for (std::size_t t = 0; t < os.size(); ++t) bad[w] += !same(s.blocks[t], os[t]);
+                try {
+                    mat_add(a, compress_matrix(field(8, 8, rng)));
+                    ++bad[w];
+                } catch (const std::invalid_argument& e) {
+                    const std::string want = "mat_add: dimension mismatch (" + std::to_string(ma.rows) + "x56 vs 8x8)";
+                    bad[w] += std::string(e.what()) != want;
+                }
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+    for (int w = 0; w < kThreads; ++w) EXPECT_EQ(bad[w], 0) << "thread " << w;
 }

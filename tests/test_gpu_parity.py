@@ -183,6 +183,30 @@ def test_addsub_rounding_ties_and_large_weights(port):
     assert np.any(phis % 2 == 0)
 
 
+def test_inplace_add_sub_with_dense_fallback(port):
+    """out may be one of the inputs (dev.add(a, b, out=a)): blocks that take the
+    s1 + s2 == 0 dense fallback still read the original records."""
+    a = W.smooth_field(96, 200, seed=31).numpy()
+    ca = dev.compress(torch.from_numpy(a).cuda())
+    neg = dev.scale(ca, -1.0)  # every block with s != 0 takes the fallback in ca + neg
+    mix = dev.compress(torch.from_numpy(W.rough_uniform(96, 200, seed=32).numpy()).cuda())
+    for op, x, y in ((dev.add, ca, neg), (dev.sub, ca, dev.scale(ca, 1.0)), (dev.add, ca, mix), (dev.sub, mix, ca)):
+        want = op(x, y)
+        for alias in (0, 1):
+            xx = dev.DeviceCMat(x.rows, x.cols, buf=x.buf.clone())
+            yy = dev.DeviceCMat(y.rows, y.cols, buf=y.buf.clone())
+            got = op(xx, yy, out=xx if alias == 0 else yy)
+            dev.sync()
+            assert _equal_cmats(got, want)
+    # a partially overlapping output is rejected (not silently corrupted)
+    big = torch.empty(ca.buf.numel() + 512, dtype=torch.uint8, device="cuda")
+    v1 = dev.DeviceCMat(ca.rows, ca.cols, buf=big)
+    v1.buf[: ca.buf.numel()].copy_(ca.buf)
+    v2 = dev.DeviceCMat(ca.rows, ca.cols, buf=big[256:])
+    with pytest.raises(blz.InvalidArgument, match="overlaps"):
+        dev.add(v1, neg, out=v2)
+
+
 def _extreme_records(n, seed):
     rng = np.random.default_rng(seed)
     rec = np.zeros(n, dtype=blz.BLOCK_DTYPE)
@@ -396,6 +420,27 @@ def test_matmul_fused_dmma_tolerance(port):
     err = np.max(np.abs(fused - exact)) / max(1.0, np.max(np.abs(exact)))
     assert err <= 1e-13 * 512, err
     assert np.array_equal(bits(fused), bits(dev.matmul_dense(A, B, mode=blz.GEMM_FUSED).cpu().numpy()))  # deterministic
+
+
+@pytest.mark.parametrize("shape", [(256, 512, 256), (200, 333, 136), (8, 1000, 24)])
+def test_matmul_fused_kernels_bitwise_equal(shape):
+    """The two fused kernels (DFMA on CUDA cores, DMMA on FP64 tensor cores) compute
+    the same ascending-k FMA chain: bitwise equal outputs, ragged shapes included,
+    and BLZ_GEMM_FUSED is one of them."""
+    m, k, n = shape
+    A = dev.compress(W.rough_uniform(m, k, seed=45, device="cuda"))
+    B = dev.compress(W.smooth_field(k, n, seed=46, device="cuda"))
+    dmma = dev.matmul_dense(A, B, mode=blz.GEMM_FUSED_DMMA).cpu().numpy()
+    dfma = dev.matmul_dense(A, B, mode=blz.GEMM_FUSED_DFMA).cpu().numpy()
+    fused = dev.matmul_dense(A, B, mode=blz.GEMM_FUSED).cpu().numpy()
+    assert np.array_equal(bits(dmma), bits(dfma))
+    assert np.array_equal(bits(fused), bits(dfma))
+    c_dmma = dev.matmul(A, B, mode=blz.GEMM_FUSED_DMMA)
+    c_dfma = dev.matmul(A, B, mode=blz.GEMM_FUSED_DFMA)
+    dev.sync()
+    assert _equal_cmats(c_dmma, c_dfma)
+    with pytest.raises(blz.InvalidArgument, match="bad mode"):
+        dev.matmul_dense(A, B, mode=7)
 
 
 # ---- .blzc container (SURVEY.md 8f-1; H/io.hpp:93-134) --------------------------
