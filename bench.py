@@ -42,7 +42,7 @@ BYTES = {  # algorithmic bytes per 8x8 block
     "decompress": 45 + 512,
     "add": 90 + 45,
     "sub": 90 + 45,
-    "scale": 45 + 45,
+    "scale": 16 + 16,  # metadata-only: f, s read and written; phi / C aliased (32 if aliased)
 }
 CONFIGS = {
     "cfg0": dict(rows=1024, cols=1024, gen="smooth"),
@@ -287,14 +287,15 @@ def run_ours(args, cfg, rank, world, local):
     B = W.make(cfg["gen"], rows, cols, seed=2 + 1000 * rank, device="cuda")
     ctx = dev.context(local)
     cA, cB = dev.DeviceCMat(rows, cols), dev.DeviceCMat(rows, cols)
-    cS, cD, cK = (dev.DeviceCMat(rows, cols) for _ in range(3))
+    cS, cD = (dev.DeviceCMat(rows, cols) for _ in range(2))
+    cK = dev.ScaledCMat(cA)  # 3.5*A: own f / s, phi / C shared with A (metadata-only scale)
     oS, oD, oK = (torch.empty((rows, cols), dtype=torch.float64, device="cuda") for _ in range(3))
     stream = torch.cuda.current_stream()
     ops = ["compress", "compress", "add", "sub", "scale", "decompress", "decompress", "decompress"]
 
     def step(ev=None):
         calls = [lambda: dev.compress(A, cA), lambda: dev.compress(B, cB), lambda: dev.add(cA, cB, cS),
-                 lambda: dev.sub(cA, cB, cD), lambda: dev.scale(cA, 3.5, cK), lambda: dev.decompress(cS, oS),
+                 lambda: dev.sub(cA, cB, cD), lambda: dev.scale_meta(cA, 3.5, cK), lambda: dev.decompress(cS, oS),
                  lambda: dev.decompress(cD, oD), lambda: dev.decompress(cK, oK)]
         for n, c in enumerate(calls):
             c()
@@ -313,7 +314,7 @@ def run_ours(args, cfg, rank, world, local):
         ea.record(stream)
         with torch.cuda.stream(s3):
             s3.wait_event(ea)
-            dev.scale(cA, 3.5, cK)
+            dev.scale_meta(cA, 3.5, cK)
             dev.decompress(cK, oK)
         dev.compress(B, cB)
         eb = torch.cuda.Event()
@@ -377,7 +378,7 @@ def run_ours(args, cfg, rank, world, local):
     # parity spot check of this run's outputs (sampled block-rows vs the oracle)
     parity = None
     if rank == 0 and not args.no_parity:
-        parity = spot_parity(A, B, cA, cS, oS, rows, cols)
+        parity = spot_parity(A, B, cA, cS, oS, cK, oK, rows, cols)
 
     e2e = None
     if not args.no_e2e:
@@ -709,8 +710,8 @@ def load_traffic(kernel):
     return None
 
 
-def spot_parity(A, B, cA, cS, oS, rows, cols):
-    """Bitwise check of 2 sampled block-rows of compress / add / decompress against the oracle."""
+def spot_parity(A, B, cA, cS, oS, cK, oK, rows, cols):
+    """Bitwise check of 2 sampled block-rows of compress / add / scale / decompress against the oracle."""
     import torch
 
     from oracle import oracle as O
@@ -734,6 +735,12 @@ def spot_parity(A, B, cA, cS, oS, rows, cols):
         mism += int((cS.slope[t0:t1].cpu().numpy().view(u64) != osum["slope"].reshape(-1).view(u64)).sum())
         dec = port.decompress_matrix(osum, 8, cols)
         mism += int((oS[r0:r0 + 8].cpu().numpy().view(u64) != dec.view(u64)).sum())
+        oscl = port.mat_scale(oa, 3.5)
+        mism += int((cK.first[t0:t1].cpu().numpy().view(u64) != oscl["first"].reshape(-1).view(u64)).sum())
+        mism += int((cK.slope[t0:t1].cpu().numpy().view(u64) != oscl["slope"].reshape(-1).view(u64)).sum())
+        mism += int((cK.coeffs[t0:t1].cpu().numpy() != oscl["coeffs"].reshape(-1, 28)).sum())
+        deck = port.decompress_matrix(oscl, 8, cols)
+        mism += int((oK[r0:r0 + 8].cpu().numpy().view(u64) != deck.view(u64)).sum())
     res["sampled_block_rows"] = 2
     res["mismatches"] = mism
     res["bit_exact"] = mism == 0

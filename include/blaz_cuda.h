@@ -134,6 +134,12 @@ blz_status blz_decompress_dev(blz_ctx* ctx, const blz_cmat* in, double* dense, u
 blz_status blz_add_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out);
 blz_status blz_sub_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out);
 blz_status blz_scale_dev(blz_ctx* ctx, const blz_cmat* a, double c, const blz_cmat* out);
+/* mat_scale as a metadata-only update (H/block_ops.hpp:74-77
+ * changes only f and s): writes out->first / out->slope (c * a's) and points
+ * out->scale / out->coeffs at a's arrays, so 16 B/block are read and 16 B
+ * written instead of 45 + 45.  The result shares a's phi/C storage: it is valid
+ * while a's arrays are alive and unchanged.  out may be a itself (in place). */
+blz_status blz_scale_meta_dev(blz_ctx* ctx, const blz_cmat* a, double c, blz_cmat* out);
 /* Fused op chains: the op of blz_add_dev / blz_sub_dev /
  * blz_scale_dev writing `out`, followed by blz_decompress_dev(out, dense, ld),
  * in one pass over the operands; results are bitwise those of the two calls.

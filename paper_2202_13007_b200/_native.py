@@ -81,6 +81,7 @@ SIGNATURES = {
     "blz_add_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_sub_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_scale_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
+    "blz_scale_meta_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
     "blz_allgather_cmat_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_rowdot_frobenius_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _U64, _P, _P]),
     "blz_frobenius_allreduce_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _P]),
@@ -139,7 +140,10 @@ def load(path: str | None = None):
     if not os.path.exists(path):
         raise NotBuilt(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = C.CDLL(path)
+    ab = path != LIB_PATH  # an A/B build of an older revision may lack newer entry points
     for name, (res, args) in SIGNATURES.items():
+        if ab and not hasattr(lib, name):
+            continue
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

@@ -210,6 +210,44 @@ __global__ void __launch_bounds__(256) k_scale_v2(CMat a, double c, CMat out) {
   for (uint64_t i = np * 16 + tid; i < nb; i += nth) out.scale[i] = a.scale[i];
 }
 
+// metadata-only mat_scale (H/block_ops.hpp:74-77 touches only f and s): two
+// flat f64 streams, 16 B per block read and written (phi / C are aliased).
+__global__ void __launch_bounds__(256) k_scale_fs(const double* __restrict__ f, const double* __restrict__ s, double c,
+                                                  double* __restrict__ fo, double* __restrict__ so, uint64_t nb) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(f) | reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(fo) |
+                     reinterpret_cast<uintptr_t>(so)) & 15) == 0;
+  if (vec) {
+    const uint64_t n2 = nb / 2;
+    for (uint64_t i = tid; i < n2; i += nth) {
+      const double2 a = reinterpret_cast<const double2*>(f)[i];
+      const double2 b = reinterpret_cast<const double2*>(s)[i];
+      reinterpret_cast<double2*>(fo)[i] = make_double2(a.x * c, a.y * c);
+      reinterpret_cast<double2*>(so)[i] = make_double2(b.x * c, b.y * c);
+    }
+    if ((nb & 1) && tid == 0) {
+      fo[nb - 1] = f[nb - 1] * c;
+      so[nb - 1] = s[nb - 1] * c;
+    }
+  } else {
+    for (uint64_t i = tid; i < nb; i += nth) {
+      fo[i] = f[i] * c;
+      so[i] = s[i] * c;
+    }
+  }
+}
+
+cudaError_t launch_scale_fs(const LaunchCtx& c, const double* f, const double* s, double k, double* fo, double* so,
+                            uint64_t nb) {
+  const uint64_t want = (nb / 2 + 255) / 256;
+  const uint64_t cap = (uint64_t)c.sm_count * SCL_GRID_PER_SM;
+  const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+  k_scale_fs<<<g, 256, 0, c.stream>>>(f, s, k, fo, so, nb);
+  ++*c.launches;
+  return cudaGetLastError();
+}
+
 static bool soa_aligned(const CMat& m) {
   return ((reinterpret_cast<uintptr_t>(m.first) | reinterpret_cast<uintptr_t>(m.slope) |
            reinterpret_cast<uintptr_t>(m.coeffs) | reinterpret_cast<uintptr_t>(m.scale)) & 15) == 0;

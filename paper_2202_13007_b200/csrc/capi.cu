@@ -457,6 +457,22 @@ blz_status blz_scale_dev(blz_ctx* c, const blz_cmat* a, double k, const blz_cmat
   return cuda_err(c, blz::launch_scale(lc(c), view(a), k, view(out)), "mat_scale");
 }
 
+blz_status blz_scale_meta_dev(blz_ctx* c, const blz_cmat* a, double k, blz_cmat* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "mat_scale")) return st;
+  if (!out) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_scale: null matrix");
+  if (out->rows != a->rows || out->cols != a->cols || out->block_rows != a->block_rows ||
+      out->block_cols != a->block_cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "mat_scale: output dimension mismatch");
+  const uint64_t nb = a->block_rows * a->block_cols;
+  if (nb && (!out->first || !out->slope)) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_scale: null buffer");
+  if (nb == 0) return BLZ_OK;
+  if (!std::isfinite(k)) return set_err(c, BLZ_INVALID_ARGUMENT, "scale: non-finite constant");  // H/block_ops.hpp:75
+  out->scale = a->scale;
+  out->coeffs = a->coeffs;
+  return cuda_err(c, blz::launch_scale_fs(lc(c), a->first, a->slope, k, out->first, out->slope, nb), "mat_scale");
+}
+
 // Fused op + decompress: out receives the compressed result
 // (as blz_add_dev / blz_sub_dev / blz_scale_dev) and dense its decompression
 // (as blz_decompress_dev), bitwise equal to the two-call chain.

@@ -185,12 +185,40 @@ __global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a,
   }
 }
 
-__global__ void k_sum(const double* __restrict__ v, uint64_t n, double* __restrict__ out) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double s = 0.0;
-    for (uint64_t k = 0; k < n; ++k) s += v[k];
-    *out = s;
+// Ascending serial sum from +0.0 (the restated oracle's order; inherently one
+// dependent DADD chain).  One warp: lanes load 32 consecutive values per step
+// (coalesced, several steps in flight), lane 0 adds them in order from
+// registers via shuffles, so the chain runs at the DADD latency instead of the
+// load latency.
+__global__ void __launch_bounds__(32) k_sum(const double* __restrict__ v, uint64_t n, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  constexpr int AHEAD = 8;
+  double buf[AHEAD];
+  const uint64_t steps = (n + 31) / 32;
+#pragma unroll
+  for (int k = 0; k < AHEAD; ++k) {
+    const uint64_t i = (uint64_t)k * 32 + lane;
+    buf[k] = i < n ? v[i] : 0.0;
   }
+  for (uint64_t st = 0; st < steps; st += AHEAD) {
+#pragma unroll
+    for (int k = 0; k < AHEAD; ++k) {
+      const double x = buf[k];
+      const uint64_t nx = (st + k + AHEAD) * 32 + lane;
+      buf[k] = nx < n ? v[nx] : 0.0;
+      const uint64_t base = (st + k) * 32;
+      if (base < n) {
+        const int cnt = n - base < 32 ? (int)(n - base) : 32;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const double y = __shfl_sync(0xffffffffu, x, q);
+          if (q < cnt) s += y;
+        }
+      }
+    }
+  }
+  if (lane == 0) *out = s;
 }
 
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,

@@ -53,6 +53,9 @@ cudaError_t launch_unpack_aos(const LaunchCtx& c, const void* aos, const CMat& o
 // addsub.cu (coalesced warp-staged variants; false if the SoA arrays are not 16-byte aligned)
 bool launch_addsub_v2(const LaunchCtx& c, bool sub, const CMat& a, const CMat& b, const CMat& out, cudaError_t* err);
 bool launch_scale_v2(const LaunchCtx& c, const CMat& a, double k, const CMat& out, cudaError_t* err);
+// metadata-only scale: f and s (phi / C are shared with the input)
+cudaError_t launch_scale_fs(const LaunchCtx& c, const double* f, const double* s, double k, double* fo, double* so,
+                            uint64_t nb);
 // io.cu (.blzc container)
 cudaError_t launch_pack_blzc(const LaunchCtx& c, const CMat& in, uint8_t* out);
 cudaError_t launch_unpack_blzc(const LaunchCtx& c, const uint8_t* in, const CMat& out, uint64_t nlimit);

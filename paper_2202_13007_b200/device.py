@@ -157,6 +157,51 @@ def scale(a: DeviceCMat, c: float, out: DeviceCMat | None = None) -> DeviceCMat:
     return out
 
 
+class ScaledCMat(DeviceCMat):
+    """Result of `scale_meta`: own f / s arrays, phi / C shared with the source
+    matrix (kept alive by this object)."""
+
+    def __init__(self, a: DeviceCMat, fs: torch.Tensor | None = None):
+        nb = a.nblocks
+        self.rows, self.cols = a.rows, a.cols
+        self.src = a
+        self.buf = fs if fs is not None else torch.empty(max(2 * nb, 2), dtype=torch.float64, device=a.buf.device)
+        assert self.buf.dtype == torch.float64 and self.buf.numel() >= 2 * nb
+        self.c = N.blz_cmat()
+        self.c.rows, self.c.cols = a.rows, a.cols
+        self.c.block_rows, self.c.block_cols = a.block_rows, a.block_cols
+        self.c.first = self.buf.data_ptr()
+        self.c.slope = self.buf.data_ptr() + 8 * nb
+        self.c.scale, self.c.coeffs = a.c.scale, a.c.coeffs
+
+    @property
+    def first(self):
+        return self.buf[: self.nblocks]
+
+    @property
+    def slope(self):
+        return self.buf[self.nblocks: 2 * self.nblocks]
+
+    @property
+    def scale(self):
+        return self.src.scale
+
+    @property
+    def coeffs(self):
+        return self.src.coeffs
+
+
+def scale_meta(a: DeviceCMat, c: float, out: ScaledCMat | None = None) -> ScaledCMat:
+    """mat_scale as a metadata-only update (H/block_ops.hpp:74-77 changes only f
+    and s): 16 B/block read and written; phi / C stay in `a`'s arrays."""
+    ctx = context(a.buf.device.index)
+    out = out if out is not None else ScaledCMat(a)
+    if out.src is not a:
+        out.src = a
+    ctx.check(ctx.lib.blz_scale_meta_dev(ctx.handle, a.ref(), C.c_double(c), out.ref()))
+    return out
+
+
 def _dense_for(a: DeviceCMat, dense: torch.Tensor | None) -> torch.Tensor:
     if dense is None:
         dense = torch.empty((a.rows, a.cols), dtype=torch.float64, device=a.buf.device)

@@ -207,6 +207,26 @@ def test_inplace_add_sub_with_dense_fallback(port):
         dev.add(v1, neg, out=v2)
 
 
+def test_scale_metadata_only(port):
+    """blz_scale_meta_dev (f and s only, phi / C aliased to the input) equals
+    mat_scale bitwise, decompresses identically, and keeps the reference's error."""
+    a = W.quadratic_blocks(200, 136, seed=33).numpy()
+    ca = dev.compress(torch.from_numpy(a).cuda())
+    for c in (3.5, -1.0, 0.0, 1e-300, -7.25e12):
+        full = dev.scale(ca, c)
+        meta = dev.scale_meta(ca, c)
+        dev.sync()
+        assert meta.c.coeffs == ca.c.coeffs and meta.c.scale == ca.c.scale  # aliased, not copied
+        assert _equal_cmats(meta, full)
+        want = port.mat_scale(ca.to_host().blocks, c)
+        assert blocks_equal(meta.to_host().blocks, want)
+        d1, d2 = dev.decompress(meta), dev.decompress(full)
+        dev.sync()
+        assert torch.equal(d1.view(torch.int64), d2.view(torch.int64))
+    with pytest.raises(blz.InvalidArgument, match="scale: non-finite constant"):
+        dev.scale_meta(ca, float("inf"))
+
+
 def _extreme_records(n, seed):
     rng = np.random.default_rng(seed)
     rec = np.zeros(n, dtype=blz.BLOCK_DTYPE)
@@ -217,6 +237,37 @@ def _extreme_records(n, seed):
     rec["scale_factor"] = np.array([1, 2, 3, 127, 128, 254, 255], dtype=np.uint8)[rng.integers(0, 7, n)]
     rec["coeffs"] = rng.integers(-127, 128, size=(n, 28)).astype(np.int8)
     return rec
+
+
+def test_decompress_magnitude_boundaries(port):
+    """Records with tiny / subnormal / huge / non-finite f and s and every
+    scale-factor class (phi = 0 included) decompress bitwise like the oracle
+    (NaN payloads aside)."""
+    rng = np.random.default_rng(77)
+    fs = [0.0, -0.0, 2.0 ** -955, -(2.0 ** -955), 2.0 ** -956, 3.1 * 2.0 ** -956, 2.0 ** -1000, 5e-324, 1.0, -7.5,
+          1e300, -1.7e308]
+    ss = [0.0, -0.0, 2.0 ** -834, -(2.0 ** -834), 2.0 ** -835, 1.9 * 2.0 ** -835, 2.0 ** -900, 1e-320, 1.0,
+          -3.25, 1e200, np.inf, np.nan]
+    recs = []
+    for f in fs:
+        for sl in ss:
+            for phi in (0, 1, 2, 77, 254, 255):
+                r = np.zeros(1, blz.BLOCK_DTYPE)
+                r["first"], r["slope"], r["scale_factor"] = f, sl, phi
+                r["coeffs"] = rng.integers(-127, 128, size=(1, 28)).astype(np.int8)
+                recs.append(r)
+    ra = np.concatenate(recs)
+    n = ra.size - ra.size % 8
+    ra = ra[:n]
+    rows, cols = 8 * (n // 8), 64
+    got = blz.decompress_matrix(blz.CompressedMatrix(rows, cols, ra.reshape(n // 8, 8)))
+    want = port.decompress_matrix(ra, rows, cols)
+    same = np.array_equal(bits(got), bits(want))
+    if not same:  # NaN payloads may differ between x86 and the GPU; compare NaN positions and other bits
+        g, w = np.asarray(got), np.asarray(want)
+        assert np.array_equal(np.isnan(g), np.isnan(w))
+        m = ~np.isnan(w)
+        assert np.array_equal(bits(g[m]), bits(w[m]))
 
 
 def test_records_with_extreme_values(port):

@@ -1,6 +1,7 @@
-"""Runs the compressed matmul once in each mode (for ncu captures of k_gemm_exact / k_gemm_dmma).
+"""Runs the compressed matmul in each GEMM mode (ncu captures of k_gemm_simt / k_gemm_dmma),
+and with --time prints CUDA-event ms and TFLOP/s per mode.
 
-    python tools/profile_gemm.py [--n 4096]
+    python tools/profile_gemm.py [--n 4096] [--time] [--reps 3]
 """
 import argparse
 import os
@@ -14,12 +15,28 @@ from paper_2202_13007_b200 import workloads as W  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=4096)
+ap.add_argument("--time", action="store_true")
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--modes", default="0,2,3")
 a = ap.parse_args()
 A = dev.compress(W.make("smooth", a.n, a.n, seed=1, device="cuda"))
 B = dev.compress(W.make("smooth", a.n, a.n, seed=2, device="cuda"))
 scratch = dev.matmul_scratch(A, B)
-for mode in (0, 1):
-    dev.matmul(A, B, mode=mode, scratch=scratch)
+C = dev.DeviceCMat(a.n, a.n)
+names = {0: "exact (DMUL+DADD)", 1: "fused (default)", 2: "fused DMMA", 3: "fused DFMA"}
+for mode in (int(m) for m in a.modes.split(",")):
+    D = dev.matmul_dense(A, B, mode=mode, scratch=scratch)  # the GEMM alone (dense out)
+    if a.time:
+        dev.sync()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        for _ in range(a.reps):
+            dev.matmul_dense(A, B, mode=mode, out=D, scratch=scratch)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / a.reps
+        print(f"{names[mode]}: matmul_dense {a.n}^3 {ms:.3f} ms {2 * a.n ** 3 / ms / 1e9:.2f} TFLOP/s", flush=True)
+    dev.matmul(A, B, mode=mode, out=C, scratch=scratch)
 dev.sync()
 torch.cuda.synchronize()
 print("ok")

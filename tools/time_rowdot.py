@@ -16,7 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=65536)
 ap.add_argument("--reps", type=int, default=3)
 args = ap.parse_args()
-A, _ = bench._chunked_compress("smooth", args.n, args.n, 11)
-B, _ = bench._chunked_compress("smooth", args.n, args.n, 12)
-ms = bench._time(lambda: dev.frobenius(A, B), reps=args.reps)
+A, _ = bench._shard_compress("smooth", 0, args.n, args.n, 11)
+B, _ = bench._shard_compress("smooth", 0, args.n, args.n, 12)
+ms = bench._time_dist(lambda: dev.frobenius(A, B), args.reps, 1)
 print(json.dumps({"lib": os.environ.get("BLZ_LIB_PATH", "in-tree"), "n": args.n, "frobenius_ms": round(ms, 3)}))
