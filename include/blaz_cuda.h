@@ -232,6 +232,19 @@ blz_status blz_decompress_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, 
 /* dequantize_prediction (H/codec.hpp:150-158): the 8x8 slope grid of each block. */
 blz_status blz_dequantize_blocks(blz_ctx* ctx, const blz_block* in, uint64_t n, double* tiles);
 
+/* Device-batched block-level API (H/block_ops.hpp:87-142):
+ * the n = rows/8-by-cols/8 blocks of `in` (or block pairs of a, b with equal
+ * grids) in block order, results as n row-major 8x8 tiles (64 doubles each) in
+ * device memory.
+ *   reconstruct_rows(b, last_row): rows 0..last_row of decompress_block(b)
+ *     (bitwise), other rows +0.0; last_row outside [0, 7] -> BLZ_OUT_OF_RANGE
+ *     "reconstruct_rows: row index out of range"
+ *   reconstruct_cols(b, last_col): columns 0..last_col, other columns +0.0
+ *   block_mul(b1, b2): out(i,j) = sum_k d1(i,k) * d2(k,j), k ascending (= dot). */
+blz_status blz_reconstruct_rows_dev(blz_ctx* ctx, const blz_cmat* in, int last_row, double* tiles);
+blz_status blz_reconstruct_cols_dev(blz_ctx* ctx, const blz_cmat* in, int last_col, double* tiles);
+blz_status blz_block_mul_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, double* tiles);
+
 /* ---- stage functions of the codec, batched ---------------
  * Host arrays of n blocks (64 doubles each, row-major), computed on the GPU one
  * thread per block in the reference's order:

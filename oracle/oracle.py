@@ -99,6 +99,9 @@ class Port:
         self._mmd = L.fn("mat_mul_dense", C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _P])
         self._mm = L.fn("mat_mul", C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _P])
         self._rowdot = L.fn("rowdot", C.c_int, [_P, _P, _SZ, _SZ, _P])
+        self._rrows = L.fn("reconstruct_rows", None, [_P, C.c_int, _P])
+        self._rcols = L.fn("reconstruct_cols", None, [_P, C.c_int, _P])
+        self._bmul = L.fn("block_mul", None, [_P, _P, _P])
         self._sum = L.fn("sum_ascending", C.c_double, [_P, _SZ])
 
     # block level
@@ -163,6 +166,26 @@ class Port:
         a = np.array([a], BLOCK_DTYPE)
         b = np.array([b], BLOCK_DTYPE)
         return self._dot(_ptr(a), _ptr(b), i, j)
+
+    def reconstruct_rows(self, b, last_row: int) -> np.ndarray:
+        """partial_reconstruction.values (H/block_ops.hpp:87-95): rows > last_row stay +0.0."""
+        b = np.array([b], BLOCK_DTYPE)
+        out = np.zeros(64, np.float64)
+        self._rrows(_ptr(b), last_row, _ptr(out))
+        return out.reshape(8, 8)
+
+    def reconstruct_cols(self, b, last_col: int) -> np.ndarray:
+        b = np.array([b], BLOCK_DTYPE)
+        out = np.zeros(64, np.float64)
+        self._rcols(_ptr(b), last_col, _ptr(out))
+        return out.reshape(8, 8)
+
+    def block_mul(self, a, b) -> np.ndarray:
+        a = np.array([a], BLOCK_DTYPE)
+        b = np.array([b], BLOCK_DTYPE)
+        out = np.zeros(64, np.float64)
+        self._bmul(_ptr(a), _ptr(b), _ptr(out))
+        return out.reshape(8, 8)
 
     # matrix level
     def compress_matrix(self, m: np.ndarray) -> np.ndarray:

@@ -82,6 +82,9 @@ SIGNATURES = {
     "blz_sub_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_scale_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
     "blz_scale_meta_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
+    "blz_reconstruct_rows_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_int, _P]),
+    "blz_reconstruct_cols_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_int, _P]),
+    "blz_block_mul_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P]),
     "blz_allgather_cmat_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_rowdot_frobenius_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _U64, _P, _P]),
     "blz_frobenius_allreduce_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _P]),

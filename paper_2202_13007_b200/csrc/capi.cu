@@ -473,6 +473,39 @@ blz_status blz_scale_meta_dev(blz_ctx* c, const blz_cmat* a, double k, blz_cmat*
   return cuda_err(c, blz::launch_scale_fs(lc(c), a->first, a->slope, k, out->first, out->slope, nb), "mat_scale");
 }
 
+// ---- device-batched block-level API (H/block_ops.hpp:87-142) ----------------
+static blz_status reconstruct_dev(blz_ctx* c, bool cols, const blz_cmat* in, int last, double* tiles) {
+  const char* what = cols ? "reconstruct_cols" : "reconstruct_rows";
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, in, what)) return st;
+  if (last < 0 || last >= 8)  // H/block_ops.hpp:88-89, :101-102
+    return set_err(c, BLZ_OUT_OF_RANGE,
+                   std::string(what) + (cols ? ": column index out of range" : ": row index out of range"));
+  const uint64_t nb = in->block_rows * in->block_cols;
+  if (nb == 0) return BLZ_OK;
+  if (!tiles) return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": null output");
+  return cuda_err(c, blz::launch_reconstruct(lc(c), c->basis, cols, view(in), last, tiles), what);
+}
+
+blz_status blz_reconstruct_rows_dev(blz_ctx* c, const blz_cmat* in, int last_row, double* tiles) {
+  return reconstruct_dev(c, false, in, last_row, tiles);
+}
+blz_status blz_reconstruct_cols_dev(blz_ctx* c, const blz_cmat* in, int last_col, double* tiles) {
+  return reconstruct_dev(c, true, in, last_col, tiles);
+}
+
+blz_status blz_block_mul_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, double* tiles) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "block_mul")) return st;
+  if (blz_status st = check_cmat(c, b, "block_mul")) return st;
+  if (a->block_rows != b->block_rows || a->block_cols != b->block_cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "block_mul: block grids differ");
+  const uint64_t nb = a->block_rows * a->block_cols;
+  if (nb == 0) return BLZ_OK;
+  if (!tiles) return set_err(c, BLZ_INVALID_ARGUMENT, "block_mul: null output");
+  return cuda_err(c, blz::launch_block_mul(lc(c), c->basis, view(a), view(b), tiles), "block_mul");
+}
+
 // Fused op + decompress: out receives the compressed result
 // (as blz_add_dev / blz_sub_dev / blz_scale_dev) and dense its decompression
 // (as blz_decompress_dev), bitwise equal to the two-call chain.

@@ -53,6 +53,10 @@ cudaError_t launch_unpack_aos(const LaunchCtx& c, const void* aos, const CMat& o
 // addsub.cu (coalesced warp-staged variants; false if the SoA arrays are not 16-byte aligned)
 bool launch_addsub_v2(const LaunchCtx& c, bool sub, const CMat& a, const CMat& b, const CMat& out, cudaError_t* err);
 bool launch_scale_v2(const LaunchCtx& c, const CMat& a, double k, const CMat& out, cudaError_t* err);
+// blockops.cu (batched block-level API)
+cudaError_t launch_reconstruct(const LaunchCtx& c, const Basis& B, bool cols, const CMat& in, int last,
+                               double* tiles);
+cudaError_t launch_block_mul(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* tiles);
 // metadata-only scale: f and s (phi / C are shared with the input)
 cudaError_t launch_scale_fs(const LaunchCtx& c, const double* f, const double* s, double k, double* fo, double* so,
                             uint64_t nb);

@@ -271,6 +271,34 @@ def frobenius(a: DeviceCMat, b: DeviceCMat):
     return r, sum_ascending(r)
 
 
+def _tiles(cm: DeviceCMat) -> torch.Tensor:
+    return torch.empty((cm.nblocks, 8, 8), dtype=torch.float64, device=cm.buf.device)
+
+
+def reconstruct_rows(cm: DeviceCMat, last_row: int) -> torch.Tensor:
+    """partial_reconstruction.values of every block (H/block_ops.hpp:87-95): (n, 8, 8)."""
+    ctx = context(cm.buf.device.index)
+    out = _tiles(cm)
+    ctx.check(ctx.lib.blz_reconstruct_rows_dev(ctx.handle, cm.ref(), int(last_row), _ptr(out)))
+    return out
+
+
+def reconstruct_cols(cm: DeviceCMat, last_col: int) -> torch.Tensor:
+    """partial_reconstruction.values of every block (H/block_ops.hpp:99-115): (n, 8, 8)."""
+    ctx = context(cm.buf.device.index)
+    out = _tiles(cm)
+    ctx.check(ctx.lib.blz_reconstruct_cols_dev(ctx.handle, cm.ref(), int(last_col), _ptr(out)))
+    return out
+
+
+def block_mul(a: DeviceCMat, b: DeviceCMat) -> torch.Tensor:
+    """block_mul of every block pair (H/block_ops.hpp:131-142): (n, 8, 8)."""
+    ctx = context(a.buf.device.index)
+    out = _tiles(a)
+    ctx.check(ctx.lib.blz_block_mul_dev(ctx.handle, a.ref(), b.ref(), _ptr(out)))
+    return out
+
+
 def matmul_scratch(a: DeviceCMat, b: DeviceCMat) -> torch.Tensor:
     n = int(N.load().blz_matmul_scratch_bytes(a.ref(), b.ref()))
     return torch.empty(n, dtype=torch.uint8, device=a.buf.device)

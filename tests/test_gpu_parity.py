@@ -227,6 +227,32 @@ def test_scale_metadata_only(port):
         dev.scale_meta(ca, float("inf"))
 
 
+@pytest.mark.parametrize("gen", ["smooth", "rough"])
+def test_batched_block_api_matches_oracle(port, gen):
+    """blz_reconstruct_rows_dev / _cols_dev / blz_block_mul_dev over every block
+    (pair) of two matrices equal the reference's single-block functions
+    (H/block_ops.hpp:87-142) bitwise; dot(b1, b2, i, j) is block_mul's (i, j)."""
+    a = W.make(gen, 72, 40, seed=91).numpy()
+    b = W.make(gen, 72, 40, seed=92).numpy()
+    A, B = dev.compress(torch.from_numpy(a).cuda()), dev.compress(torch.from_numpy(b).cuda())
+    ha, hb = A.to_host().blocks.reshape(-1), B.to_host().blocks.reshape(-1)
+    for last in (0, 3, 7):
+        rr = dev.reconstruct_rows(A, last).cpu().numpy()
+        rc = dev.reconstruct_cols(A, last).cpu().numpy()
+        for t in range(ha.size):
+            assert np.array_equal(bits(rr[t]), bits(port.reconstruct_rows(ha[t], last))), (last, t)
+            assert np.array_equal(bits(rc[t]), bits(port.reconstruct_cols(ha[t], last))), (last, t)
+    bm = dev.block_mul(A, B).cpu().numpy()
+    for t in range(ha.size):
+        want = port.block_mul(ha[t], hb[t])
+        assert np.array_equal(bits(bm[t]), bits(want)), t
+        assert np.float64(bm[t][2, 5]).view(np.uint64) == np.float64(port.dot(ha[t], hb[t], 2, 5)).view(np.uint64)
+    with pytest.raises(blz.OutOfRange, match="reconstruct_rows: row index out of range"):
+        dev.reconstruct_rows(A, 8)
+    with pytest.raises(blz.OutOfRange, match="reconstruct_cols: column index out of range"):
+        dev.reconstruct_cols(A, -1)
+
+
 def _extreme_records(n, seed):
     rng = np.random.default_rng(seed)
     rec = np.zeros(n, dtype=blz.BLOCK_DTYPE)
