@@ -786,25 +786,78 @@ def run_e2e(args, A, B, rows, cols, nb, world):
             ctx.check(lib.blz_decompress_matrix(h, P(c), rows, cols, P(d), 0))
 
     pinned = (npA, npB, cA, cB, cS, cD, cK, dS, dD, dK)
+    # The same calls issued as the op graph from two host threads, each with its own
+    # context (the drop-in's per-thread contexts): compress(B)'s upload overlaps
+    # decompress(3.5 A)'s download, add -> decompress and sub -> decompress run side by
+    # side.  Results are those of the sequential order (the calls are independent).
+    import threading
+    ctx2 = blz.Context(torch.cuda.current_device())
+    dS2 = pinned_dense()  # the second thread's decompressed results
+
+    def step_dag(xA, xB, bA, bB, bS, bD, bK, d1, d2):
+        h1, h2 = h, ctx2.handle
+        ready = threading.Event()
+        err = []
+
+        def t2():
+            try:
+                ready.wait()
+                ctx2.check(lib.blz_compress_matrix(h2, P(xB), rows, cols, P(bB), 0))
+            except Exception as e:  # re-raised by the caller
+                err.append(e)
+        th = threading.Thread(target=t2)
+        th.start()
+        ctx.check(lib.blz_compress_matrix(h1, P(xA), rows, cols, P(bA), 0))
+        ready.set()
+        ctx.check(lib.blz_mat_scale(h1, P(bA), rows, cols, 3.5, P(bK), 0))
+        ctx.check(lib.blz_decompress_matrix(h1, P(bK), rows, cols, P(d1), 0))
+        th.join()
+        if err:
+            raise err[0]
+
+        def t3():
+            try:
+                ctx2.check(lib.blz_mat_sub(h2, P(bA), rows, cols, P(bB), rows, cols, P(bD), 0))
+                ctx2.check(lib.blz_decompress_matrix(h2, P(bD), rows, cols, P(d2), 0))
+            except Exception as e:
+                err.append(e)
+        th = threading.Thread(target=t3)
+        th.start()
+        ctx.check(lib.blz_mat_add(h1, P(bA), rows, cols, P(bB), rows, cols, P(bS), 0))
+        ctx.check(lib.blz_decompress_matrix(h1, P(bS), rows, cols, P(d1), 0))
+        th.join()
+        if err:
+            raise err[0]
+
+    dag = (npA, npB, cA, cB, cS, cD, cK, dS, dS2)
     step(*pinned)  # warm-up (scratch allocation)
+    step_dag(*dag)
     torch.cuda.synchronize()
     n = max(1, min(args.steps, args.e2e_steps))
-    barrier(world)
-    t0 = time.perf_counter()
-    for _ in range(n):
-        step(*pinned)
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / n
-    dt = max_over_ranks(dt, world)
     dense, blk = rows * cols * 8, nb * 48
     h2d = 2 * dense + 2 * (2 * blk) + blk + 3 * blk
     d2h = 2 * blk + 3 * blk + 3 * dense
+
+    def timed(fn, bufs, reps):
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn(*bufs)
+        torch.cuda.synchronize()
+        return max_over_ranks((time.perf_counter() - t0) / reps, world)
+    dt_seq = timed(step, pinned, n)
+    dt = timed(step_dag, dag, n)
     res = {"value": nb * world / dt, "unit": "blocks/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": dt * 1e3, "steps": n,
            "api": "C ABI host entry points blz_compress_matrix / blz_mat_add / blz_mat_sub / "
-                  "blz_mat_scale / blz_decompress_matrix (pinned host buffers)"}
+                  "blz_mat_scale / blz_decompress_matrix (pinned host buffers), issued as the op graph "
+                  "from two host threads with one context each",
+           "sequential": {"value": nb * world / dt_seq, "ms_per_step": dt_seq * 1e3,
+                          "note": "the same calls one after another from one thread"}}
+    ctx2.close()
+    del dS2
     # the drop-in's usual case: pageable std::vector-like buffers (plain numpy arrays)
-    del hA, hB, cA, cB, cS, cD, cK, dS, pinned
+    del hA, hB, cA, cB, cS, cD, cK, dS, pinned, dag
     pA, pB = np.array(npA), np.array(npB)
     del npA, npB
     pbl = [np.zeros((nbr, nbc), blz.BLOCK_DTYPE) for _ in range(5)]

@@ -21,6 +21,7 @@ static_assert(sizeof(blz_block) == 48, "blz_block must match blaz::compressed_bl
 struct blz_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;  // created with the context (non-blocking); blz_ctx_set_stream may replace it
   blz::Basis basis{};
   std::string err;
   unsigned long long* d_err = nullptr;
@@ -218,7 +219,8 @@ blz_status latch_status(blz_ctx* c) {
   BLZ_CUDA(c, cudaStreamSynchronize(c->stream), "sync");
   if (v == ~0ull) return BLZ_OK;
   const unsigned long long reset = ~0ull;
-  BLZ_CUDA(c, cudaMemcpy(c->d_err, &reset, sizeof reset, cudaMemcpyHostToDevice), "error latch reset");
+  BLZ_CUDA(c, cudaMemcpyAsync(c->d_err, &reset, sizeof reset, cudaMemcpyHostToDevice, c->stream), "error latch reset");
+  BLZ_CUDA(c, cudaStreamSynchronize(c->stream), "sync");
   switch ((uint32_t)(v & 0xff)) {
     case blz::DERR_NONFINITE_CODE:
       return set_err(c, BLZ_INVALID_ARGUMENT, "normalize: non-finite input");
@@ -283,6 +285,10 @@ blz_status blz_ctx_create(int device, const double* basis, blz_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(c->d_err, 0xff, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_stats, 4 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->d_stats, 0, 4 * sizeof(unsigned long long));
+  // a private non-blocking stream: contexts of different host threads (the drop-in
+  // creates one per thread) never serialise on the legacy default stream
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) c->stream = c->own_stream;
   if (e != cudaSuccess) {
     delete c;
     return e == cudaErrorMemoryAllocation ? BLZ_OUT_OF_MEMORY : BLZ_CUDA_ERROR;
@@ -305,6 +311,10 @@ void blz_ctx_destroy(blz_ctx* c) {
   if (c->d_err) cudaFree(c->d_err);
   if (c->d_stats) cudaFree(c->d_stats);
   if (c->d_wl) cudaFree(c->d_wl);
+  if (c->own_stream) {
+    cudaStreamSynchronize(c->own_stream);
+    cudaStreamDestroy(c->own_stream);
+  }
   if (c->s_in) cudaStreamDestroy(c->s_in);
   if (c->s_out) cudaStreamDestroy(c->s_out);
   for (auto ev : c->events) cudaEventDestroy(ev);
@@ -718,6 +728,22 @@ blz_status pipelined(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compu
 // device AoS staging for block-row range [b0, b1) of a (rows x cols) grid
 blz_block* aos_at(void* base, uint64_t b0, uint64_t bc) { return (blz_block*)base + b0 * bc; }
 
+// Device alias of a page-locked (pinned / registered, mapped) host buffer, or
+// null for pageable memory.  The host entry points read their compressed-record
+// inputs and write their compressed-record outputs through this alias: the
+// unpack / pack kernels move those bytes over PCIe themselves (zero-copy), so
+// the copy engines carry only the dense matrices, and the small transfers of
+// one call never queue behind another call's large ones (calls from several
+// host threads overlap their PCIe directions).
+const void* mapped_alias(const void* host) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 }  // namespace
 
 extern "C" {
@@ -736,6 +762,7 @@ blz_status blz_compress_matrix(blz_ctx* c, const double* values, uint64_t rows, 
   void* aos = slot(c, S_AUX, m.block_rows * bc * sizeof(blz_block), &e);
   if (!aos) return cuda_err(c, e, "scratch allocation");
   if (blz_status st = ensure_worklist(c, m.block_rows * bc)) return st;
+  blz_block* out_z = (blz_block*)mapped_alias(out);
   auto rows_of = [&](uint64_t b0, uint64_t b1) { return std::min(rows, 8 * b1) - 8 * b0; };
   blz_status st = pipelined(
       c, m.block_rows,
@@ -746,9 +773,10 @@ blz_status blz_compress_matrix(blz_ctx* c, const double* values, uint64_t rows, 
       [&](uint64_t b0, uint64_t b1) {
         const blz_cmat v = sub_rows(m, b0, b1);
         if (blz_status st2 = blz_compress_dev(c, d + 8 * b0 * cols, v.rows, cols, cols, &v)) return st2;
-        return blz_pack_aos_dev(c, &v, aos_at(aos, b0, bc));
+        return blz_pack_aos_dev(c, &v, out_z ? out_z + b0 * bc : aos_at(aos, b0, bc));
       },
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        if (out_z) return cudaSuccess;  // written by the pack kernel
         return cudaMemcpyAsync(out + b0 * bc, aos_at(aos, b0, bc), (b1 - b0) * bc * sizeof(blz_block),
                                cudaMemcpyDeviceToHost, s);
       });
@@ -769,16 +797,18 @@ blz_status blz_decompress_matrix(blz_ctx* c, const blz_block* in, uint64_t rows,
   if (!aos) return cuda_err(c, e, "scratch allocation");
   double* d = (double*)slot(c, S_OUT, rows * cols * sizeof(double), &e);
   if (!d) return cuda_err(c, e, "scratch allocation");
+  const blz_block* in_z = (const blz_block*)mapped_alias(in);
   auto rows_of = [&](uint64_t b0, uint64_t b1) { return std::min(rows, 8 * b1) - 8 * b0; };
   blz_status st = pipelined(
       c, m.block_rows,
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        if (in_z) return cudaSuccess;  // read by the unpack kernel
         return cudaMemcpyAsync(aos_at(aos, b0, bc), in + b0 * bc, (b1 - b0) * bc * sizeof(blz_block),
                                cudaMemcpyHostToDevice, s);
       },
       [&](uint64_t b0, uint64_t b1) {
         const blz_cmat v = sub_rows(m, b0, b1);
-        if (blz_status st2 = blz_unpack_aos_dev(c, aos_at(aos, b0, bc), &v)) return st2;
+        if (blz_status st2 = blz_unpack_aos_dev(c, in_z ? in_z + b0 * bc : aos_at(aos, b0, bc), &v)) return st2;
         return blz_decompress_dev(c, &v, d + 8 * b0 * cols, cols);
       },
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
@@ -805,12 +835,26 @@ static blz_status elementwise_host(blz_ctx* c, int op, const blz_block* a, const
   blz_block *sa = aos, *sb = aos + nb, *so = aos + 2 * nb;
   if (op != 2)
     if (blz_status st = ensure_worklist(c, nb)) return st;
+  // the record streams of add / sub / scale go through the copy engines: both
+  // directions are records here, and staged copies measured faster than
+  // zero-copy kernel access for these calls (ZC_ELEMENTWISE=1 switches)
+#ifndef ZC_ELEMENTWISE
+#define ZC_ELEMENTWISE 0
+#endif
+  const blz_block* a_z = ZC_ELEMENTWISE ? (const blz_block*)mapped_alias(a) : nullptr;
+  const blz_block* b_z = ZC_ELEMENTWISE && op != 2 ? (const blz_block*)mapped_alias(b) : nullptr;
+  blz_block* o_z = ZC_ELEMENTWISE ? (blz_block*)mapped_alias(out) : nullptr;
+  if (a_z) sa = (blz_block*)a_z;
+  if (b_z) sb = (blz_block*)b_z;
+  if (o_z) so = o_z;
   return pipelined(
       c, ma.block_rows,
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
         const size_t n = (b1 - b0) * bc * sizeof(blz_block);
-        cudaError_t e2 = cudaMemcpyAsync(sa + b0 * bc, a + b0 * bc, n, cudaMemcpyHostToDevice, s);
-        if (e2 == cudaSuccess && op != 2) e2 = cudaMemcpyAsync(sb + b0 * bc, b + b0 * bc, n, cudaMemcpyHostToDevice, s);
+        cudaError_t e2 = cudaSuccess;
+        if (!a_z) e2 = cudaMemcpyAsync(sa + b0 * bc, a + b0 * bc, n, cudaMemcpyHostToDevice, s);
+        if (e2 == cudaSuccess && op != 2 && !b_z)
+          e2 = cudaMemcpyAsync(sb + b0 * bc, b + b0 * bc, n, cudaMemcpyHostToDevice, s);
         return e2;
       },
       [&](uint64_t b0, uint64_t b1) {
@@ -826,6 +870,7 @@ static blz_status elementwise_host(blz_ctx* c, int op, const blz_block* a, const
         return blz_pack_aos_dev(c, &vo, so + b0 * bc);
       },
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
+        if (o_z) return cudaSuccess;  // written by the pack kernel
         return cudaMemcpyAsync(out + b0 * bc, so + b0 * bc, (b1 - b0) * bc * sizeof(blz_block),
                                cudaMemcpyDeviceToHost, s);
       });

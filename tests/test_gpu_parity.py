@@ -253,6 +253,43 @@ def test_batched_block_api_matches_oracle(port, gen):
         dev.reconstruct_cols(A, -1)
 
 
+def test_host_calls_pinned_zero_copy_equal_pageable():
+    """Host entry points with page-locked buffers read / write the compressed
+    records zero-copy (kernels over PCIe); results equal the pageable path."""
+    rows, cols = 520, 392
+    a = W.smooth_field(rows, cols, seed=61).numpy()
+    b = W.quadratic_blocks(rows, cols, seed=62).numpy()
+    ctx = blz.default_context()
+    lib, h = ctx.lib, ctx.handle
+    nb = ((rows + 7) // 8) * ((cols + 7) // 8)
+
+    def pinned_like(x):
+        t = torch.empty(x.nbytes, dtype=torch.uint8, pin_memory=True).numpy().view(x.dtype).reshape(x.shape)
+        t[...] = x
+        return t
+
+    def blocks(pin):
+        z = np.zeros(nb, blz.BLOCK_DTYPE)
+        return pinned_like(z) if pin else z
+
+    out = {}
+    for pin in (False, True):
+        xa, xb = (pinned_like(a), pinned_like(b)) if pin else (a.copy(), b.copy())
+        ca, cb, cs, cd, ck = (blocks(pin) for _ in range(5))
+        dd = pinned_like(np.zeros((rows, cols))) if pin else np.zeros((rows, cols))
+        P = lambda v: v.ctypes.data  # noqa: E731
+        ctx.check(lib.blz_compress_matrix(h, P(xa), rows, cols, P(ca), 0))
+        ctx.check(lib.blz_compress_matrix(h, P(xb), rows, cols, P(cb), 0))
+        ctx.check(lib.blz_mat_add(h, P(ca), rows, cols, P(cb), rows, cols, P(cs), 0))
+        ctx.check(lib.blz_mat_sub(h, P(ca), rows, cols, P(cb), rows, cols, P(cd), 0))
+        ctx.check(lib.blz_mat_scale(h, P(ca), rows, cols, -2.25, P(ck), 0))
+        ctx.check(lib.blz_decompress_matrix(h, P(cs), rows, cols, P(dd), 0))
+        out[pin] = [x.copy() for x in (ca, cb, cs, cd, ck)] + [dd.copy()]
+    for x, y in zip(out[False][:5], out[True][:5]):
+        assert blocks_equal(x, y)
+    assert np.array_equal(bits(out[False][5]), bits(out[True][5]))
+
+
 def _extreme_records(n, seed):
     rng = np.random.default_rng(seed)
     rec = np.zeros(n, dtype=blz.BLOCK_DTYPE)
