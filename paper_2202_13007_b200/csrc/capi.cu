@@ -6,11 +6,18 @@
 // kernel launched here.
 #include <cuda_runtime.h>
 
+#include <sched.h>
+
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/blaz_cuda.h"
@@ -37,6 +44,22 @@ struct blz_ctx {
   // host-level pipelining: copy-in / copy-out streams and per-chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> events;
+  // pageable host buffers: page-locked staging slots (two per direction, grow-only)
+  struct Stage {
+    void* p = nullptr;
+    size_t bytes = 0, off = 0;
+    cudaEvent_t ev = nullptr;
+    bool busy = false;  // a copy from / into the slot is in flight (ev recorded)
+    struct Drain {
+      void* dst;
+      const void* src;
+      size_t n;
+    };
+    std::vector<Drain> drains;  // D2H: host copies still to make out of the slot
+  };
+  Stage st_in[2], st_out[2];
+  int cur = 0;  // slot of the chunk being issued
+  int stage_pieces = 1;  // H2D pieces per chunk (reservation hint)
   // grow-only device scratch slots (host-level calls, add fallback worklist)
   struct Slot {
     void* p = nullptr;
@@ -315,6 +338,11 @@ void blz_ctx_destroy(blz_ctx* c) {
     cudaStreamSynchronize(c->own_stream);
     cudaStreamDestroy(c->own_stream);
   }
+  for (auto* g : {c->st_in, c->st_out})
+    for (int k = 0; k < 2; ++k) {
+      if (g[k].p) cudaFreeHost(g[k].p);
+      if (g[k].ev) cudaEventDestroy(g[k].ev);
+    }
   if (c->s_in) cudaStreamDestroy(c->s_in);
   if (c->s_out) cudaStreamDestroy(c->s_out);
   for (auto ev : c->events) cudaEventDestroy(ev);
@@ -687,6 +715,167 @@ blz_status ensure_pipe(blz_ctx* c, size_t nev) {
   return BLZ_OK;
 }
 
+// ---- pageable host buffers ------------------------------------------------------
+// cudaMemcpyAsync from / to pageable memory is staged by the driver at a fraction
+// of the PCIe rate.  The host entry points stage pageable buffers themselves:
+// a page-locked slot per chunk and direction (two slots, alternating), filled /
+// emptied by a pool of host threads (parallel memcpy) while the copy engine
+// moves the neighbouring chunk.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  // memcpy(dst, src, n) split over the pool and the calling thread
+  void copy(void* dst, const void* src, size_t n) {
+    const size_t piece_min = size_t(4) << 20;
+    const int parts = (int)std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, n / piece_min));
+    if (parts <= 1) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    Batch b;
+    b.left = parts - 1;
+    const size_t per = (n + parts - 1) / parts;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (int k = 1; k < parts; ++k) {
+        const size_t o = k * per, m = std::min(per, n - o);
+        jobs_.push_back({(char*)dst + o, (const char*)src + o, m, &b});
+      }
+    }
+    cv_.notify_all();
+    std::memcpy(dst, src, std::min(per, n));
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.cv.wait(lk, [&] { return b.left == 0; });
+  }
+
+ private:
+  struct Batch {
+    std::mutex mu;
+    std::condition_variable cv;
+    int left = 0;
+  };
+  struct Job {
+    char* d;
+    const char* s;
+    size_t n;
+    Batch* b;
+  };
+  CopyPool() {
+    cpu_set_t set;
+    int n = (int)std::thread::hardware_concurrency();
+    if (sched_getaffinity(0, sizeof set, &set) == 0) n = CPU_COUNT(&set);
+    n = std::max(1, std::min(n, 16)) - 1;
+    for (int k = 0; k < n; ++k) workers_.emplace_back([this] { run(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void run() {
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || !jobs_.empty(); });
+        if (stop_ && jobs_.empty()) return;
+        j = jobs_.front();
+        jobs_.pop_front();
+      }
+      std::memcpy(j.d, j.s, j.n);
+      std::lock_guard<std::mutex> lk(j.b->mu);
+      if (--j.b->left == 0) j.b->cv.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::deque<Job> jobs_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool stop_ = false;
+};
+
+const void* mapped_alias(const void* host);
+bool page_locked(const void* host) { return mapped_alias(host) != nullptr; }
+
+// Grows staging slot g to at least n bytes (waits for its in-flight copy first).
+cudaError_t stage_reserve(blz_ctx::Stage& g, size_t n) {
+  if (!g.ev) {
+    cudaError_t e = cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  if (g.bytes >= n) return cudaSuccess;
+  if (g.busy) {
+    cudaError_t e = cudaEventSynchronize(g.ev);
+    if (e != cudaSuccess) return e;
+    g.busy = false;
+  }
+  if (g.p) cudaFreeHost(g.p);
+  g.p = nullptr;
+  g.bytes = 0;
+  cudaError_t e = cudaHostAlloc(&g.p, n, cudaHostAllocDefault);
+  if (e == cudaSuccess) g.bytes = n;
+  return e;
+}
+
+// H2D of one piece of the current chunk: direct from page-locked memory, or
+// through the chunk's staging slot (host copy now, DMA on s).
+cudaError_t xfer_h2d(blz_ctx* c, void* dst, const void* src, size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (page_locked(src)) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s);
+  blz_ctx::Stage& g = c->st_in[c->cur];
+  if (g.busy) {  // the slot's previous chunk is still being uploaded
+    cudaError_t e = cudaEventSynchronize(g.ev);
+    if (e != cudaSuccess) return e;
+    g.busy = false;
+  }
+  if (g.bytes < g.off + n) {
+    // the first piece of a chunk reserves room for the chunk's pieces (add / sub
+    // upload two equal ones); a piece already in the slot is in flight, so the
+    // slot cannot grow mid-chunk
+    if (g.off) return cudaErrorInvalidValue;
+    cudaError_t e = stage_reserve(g, (size_t)c->stage_pieces * n);
+    if (e != cudaSuccess) return e;
+  }
+  char* slotp = (char*)g.p + g.off;
+  CopyPool::get().copy(slotp, src, n);
+  g.off += n;
+  return cudaMemcpyAsync(dst, slotp, n, cudaMemcpyHostToDevice, s);
+}
+
+// D2H of one piece of the current chunk: direct into page-locked memory, or
+// into the chunk's staging slot, copied out by drain() once the DMA is done.
+cudaError_t xfer_d2h(blz_ctx* c, void* dst, const void* src, size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (page_locked(dst)) return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s);
+  blz_ctx::Stage& g = c->st_out[c->cur];
+  if (g.bytes < g.off + n) {
+    if (g.off) return cudaErrorInvalidValue;  // one piece per chunk and direction for D2H
+    cudaError_t e = stage_reserve(g, std::max(n, 2 * g.bytes));
+    if (e != cudaSuccess) return e;
+  }
+  char* slotp = (char*)g.p + g.off;
+  g.off += n;
+  g.drains.push_back({dst, slotp, n});
+  return cudaMemcpyAsync(slotp, src, n, cudaMemcpyDeviceToHost, s);
+}
+
+// Completes the host side of a staged D2H slot (waits for its DMA, copies out).
+cudaError_t drain(blz_ctx::Stage& g) {
+  if (g.drains.empty()) return cudaSuccess;
+  cudaError_t e = cudaEventSynchronize(g.ev);
+  for (auto& d : g.drains)
+    if (e == cudaSuccess) CopyPool::get().copy(d.dst, d.src, d.n);
+  g.drains.clear();
+  g.busy = false;
+  return e;
+}
+
 template <class H2D, class Compute, class D2H>
 blz_status pipelined_body(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compute, D2H&& d2h) {
   uint64_t step = (block_rows + 15) / 16;
@@ -700,14 +889,30 @@ blz_status pipelined_body(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& 
   for (uint64_t i = 0; i < nchunks; ++i) {
     const uint64_t b0 = i * step, b1 = std::min(block_rows, b0 + step);
     cudaEvent_t in_done = c->events[2 * i], k_done = c->events[2 * i + 1];
+    c->cur = (int)(i & 1);
+    blz_ctx::Stage& gi = c->st_in[c->cur];
+    blz_ctx::Stage& go = c->st_out[c->cur];
+    gi.off = 0;
+    go.off = 0;
     BLZ_CUDA(c, h2d(b0, b1, c->s_in), "H2D");
+    if (gi.off) {
+      BLZ_CUDA(c, cudaEventRecord(gi.ev, c->s_in), "event");
+      gi.busy = true;
+    }
     BLZ_CUDA(c, cudaEventRecord(in_done, c->s_in), "event");
     BLZ_CUDA(c, cudaStreamWaitEvent(c->stream, in_done, 0), "event");
     if (blz_status st = compute(b0, b1)) return st;
     BLZ_CUDA(c, cudaEventRecord(k_done, c->stream), "event");
     BLZ_CUDA(c, cudaStreamWaitEvent(c->s_out, k_done, 0), "event");
     BLZ_CUDA(c, d2h(b0, b1, c->s_out), "D2H");
+    if (!go.drains.empty()) {
+      BLZ_CUDA(c, cudaEventRecord(go.ev, c->s_out), "event");
+      go.busy = true;
+    }
+    // the previous chunk's staged downloads complete while this chunk's move
+    BLZ_CUDA(c, drain(c->st_out[c->cur ^ 1]), "D2H staging");
   }
+  BLZ_CUDA(c, drain(c->st_out[c->cur]), "D2H staging");
   return BLZ_OK;
 }
 
@@ -716,9 +921,15 @@ blz_status pipelined_body(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& 
 template <class H2D, class Compute, class D2H>
 blz_status pipelined(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compute, D2H&& d2h) {
   const blz_status st = pipelined_body(c, block_rows, h2d, compute, d2h);
+  c->stage_pieces = 1;
   const cudaError_t e1 = c->s_out ? cudaStreamSynchronize(c->s_out) : cudaSuccess;
   const cudaError_t e2 = c->s_in ? cudaStreamSynchronize(c->s_in) : cudaSuccess;
   const cudaError_t e3 = cudaStreamSynchronize(c->stream);
+  for (auto* g : {c->st_in, c->st_out})  // error paths: nothing staged stays pending
+    for (int k = 0; k < 2; ++k) {
+      g[k].drains.clear();
+      g[k].busy = false;
+    }
   if (st != BLZ_OK) return st;
   if (e1 != cudaSuccess) return cuda_err(c, e1, "sync");
   if (e2 != cudaSuccess) return cuda_err(c, e2, "sync");
@@ -767,8 +978,7 @@ blz_status blz_compress_matrix(blz_ctx* c, const double* values, uint64_t rows, 
   blz_status st = pipelined(
       c, m.block_rows,
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
-        return cudaMemcpyAsync(d + 8 * b0 * cols, values + 8 * b0 * cols, rows_of(b0, b1) * cols * sizeof(double),
-                               cudaMemcpyHostToDevice, s);
+        return xfer_h2d(c, d + 8 * b0 * cols, values + 8 * b0 * cols, rows_of(b0, b1) * cols * sizeof(double), s);
       },
       [&](uint64_t b0, uint64_t b1) {
         const blz_cmat v = sub_rows(m, b0, b1);
@@ -777,8 +987,7 @@ blz_status blz_compress_matrix(blz_ctx* c, const double* values, uint64_t rows, 
       },
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
         if (out_z) return cudaSuccess;  // written by the pack kernel
-        return cudaMemcpyAsync(out + b0 * bc, aos_at(aos, b0, bc), (b1 - b0) * bc * sizeof(blz_block),
-                               cudaMemcpyDeviceToHost, s);
+        return xfer_d2h(c, out + b0 * bc, aos_at(aos, b0, bc), (b1 - b0) * bc * sizeof(blz_block), s);
       });
   if (st) return st;
   return latch_status(c);
@@ -803,8 +1012,7 @@ blz_status blz_decompress_matrix(blz_ctx* c, const blz_block* in, uint64_t rows,
       c, m.block_rows,
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
         if (in_z) return cudaSuccess;  // read by the unpack kernel
-        return cudaMemcpyAsync(aos_at(aos, b0, bc), in + b0 * bc, (b1 - b0) * bc * sizeof(blz_block),
-                               cudaMemcpyHostToDevice, s);
+        return xfer_h2d(c, aos_at(aos, b0, bc), in + b0 * bc, (b1 - b0) * bc * sizeof(blz_block), s);
       },
       [&](uint64_t b0, uint64_t b1) {
         const blz_cmat v = sub_rows(m, b0, b1);
@@ -812,8 +1020,7 @@ blz_status blz_decompress_matrix(blz_ctx* c, const blz_block* in, uint64_t rows,
         return blz_decompress_dev(c, &v, d + 8 * b0 * cols, cols);
       },
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
-        return cudaMemcpyAsync(out + 8 * b0 * cols, d + 8 * b0 * cols, rows_of(b0, b1) * cols * sizeof(double),
-                               cudaMemcpyDeviceToHost, s);
+        return xfer_d2h(c, out + 8 * b0 * cols, d + 8 * b0 * cols, rows_of(b0, b1) * cols * sizeof(double), s);
       });
   if (st) return st;
   return latch_status(c);
@@ -847,14 +1054,14 @@ static blz_status elementwise_host(blz_ctx* c, int op, const blz_block* a, const
   if (a_z) sa = (blz_block*)a_z;
   if (b_z) sb = (blz_block*)b_z;
   if (o_z) so = o_z;
+  c->stage_pieces = op != 2 ? 2 : 1;
   return pipelined(
       c, ma.block_rows,
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
         const size_t n = (b1 - b0) * bc * sizeof(blz_block);
         cudaError_t e2 = cudaSuccess;
-        if (!a_z) e2 = cudaMemcpyAsync(sa + b0 * bc, a + b0 * bc, n, cudaMemcpyHostToDevice, s);
-        if (e2 == cudaSuccess && op != 2 && !b_z)
-          e2 = cudaMemcpyAsync(sb + b0 * bc, b + b0 * bc, n, cudaMemcpyHostToDevice, s);
+        if (!a_z) e2 = xfer_h2d(c, sa + b0 * bc, a + b0 * bc, n, s);
+        if (e2 == cudaSuccess && op != 2 && !b_z) e2 = xfer_h2d(c, sb + b0 * bc, b + b0 * bc, n, s);
         return e2;
       },
       [&](uint64_t b0, uint64_t b1) {
@@ -871,8 +1078,7 @@ static blz_status elementwise_host(blz_ctx* c, int op, const blz_block* a, const
       },
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
         if (o_z) return cudaSuccess;  // written by the pack kernel
-        return cudaMemcpyAsync(out + b0 * bc, so + b0 * bc, (b1 - b0) * bc * sizeof(blz_block),
-                               cudaMemcpyDeviceToHost, s);
+        return xfer_d2h(c, out + b0 * bc, so + b0 * bc, (b1 - b0) * bc * sizeof(blz_block), s);
       });
 }
 

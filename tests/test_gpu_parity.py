@@ -253,10 +253,12 @@ def test_batched_block_api_matches_oracle(port, gen):
         dev.reconstruct_cols(A, -1)
 
 
-def test_host_calls_pinned_zero_copy_equal_pageable():
+@pytest.mark.parametrize("rows,cols", [(520, 392), (2056, 4000)])
+def test_host_calls_pinned_zero_copy_equal_pageable(rows, cols):
     """Host entry points with page-locked buffers read / write the compressed
-    records zero-copy (kernels over PCIe); results equal the pageable path."""
-    rows, cols = 520, 392
+    records zero-copy (kernels over PCIe); pageable buffers go through the
+    library's page-locked staging slots (parallel host copies, several chunks at
+    the larger size); both equal each other bitwise."""
     a = W.smooth_field(rows, cols, seed=61).numpy()
     b = W.quadratic_blocks(rows, cols, seed=62).numpy()
     ctx = blz.default_context()
