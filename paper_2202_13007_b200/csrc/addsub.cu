@@ -22,6 +22,9 @@
 #ifndef ASB_GRID_PER_SM
 #define ASB_GRID_PER_SM 96  // many short CTAs beat a resident grid (6/SM: 0.142 ms, 96: 0.126 ms)
 #endif
+#ifndef ASB_MINB
+#define ASB_MINB 1
+#endif
 #ifndef SCL_GRID_PER_SM
 #define SCL_GRID_PER_SM 32
 #endif
@@ -30,7 +33,11 @@ namespace blz {
 
 // Requires 16-byte aligned SoA arrays whose block offset is a multiple of 4
 // blocks (true for every blz_cmat_view-created matrix); the launcher checks.
-template <bool SUB>
+// ALIAS: out is a or b (in-place use; the host compares the pointers).  The
+// dense fallback (k_addsub_fallback) re-reads a[t] and b[t] afterwards, so a
+// fallback lane must then leave the aliased input's record in place instead of
+// storing its (meaningless) combined record.
+template <bool SUB, bool ALIAS>
 __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uint64_t* __restrict__ wl,
                                                    unsigned long long* __restrict__ wl_count) {
   __shared__ __align__(16) WarpRecs sa[2][4], sb[2][4], so[4];
@@ -38,8 +45,8 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
   const uint64_t nb = out.nb();
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  // out must be disjoint from the inputs or identical to one of them (in place)
-  const int alias = out.first == a.first ? 1 : (out.first == b.first ? 2 : 0);
+  // out is disjoint from the inputs or identical to one of them (in place; host-checked)
+  const int alias = out.first == a.first ? 1 : 2;  // used when ALIAS
   int buf = 0;
   uint64_t t0 = gw * 32;
   if (t0 < nb) {
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
 #pragma unroll
     for (int w = 0; w < 7; ++w) oc[w] = o.c[w];
     if (fallback && t < nb) wl[atomicAdd(wl_count, 1ull)] = t;
-    if (fallback && alias != 0) {
+    if (ALIAS && fallback) {
       // k_addsub_fallback re-reads a[t] and b[t]: when out is one of the inputs
       // (in-place add/sub), that input's record must survive this store.
       const WarpRecs& keep = alias == 1 ? ra : rb;
@@ -92,7 +99,7 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
 #pragma unroll
       for (int w = 0; w < 7; ++w) ro.c[lane * 7 + w] = oc[w];
     }
-    if (slow && !fallback) {  // huge weights: the reference rounding sequence (blaz_device.cuh::clamp_coeff)
+    if (slow && !(ALIAS && fallback)) {  // huge weights: the reference rounding sequence (blaz_device.cuh::clamp_coeff)
       const uint8_t* b1 = reinterpret_cast<const uint8_t*>(&ra.c[lane * 7]);
       const uint8_t* b2 = reinterpret_cast<const uint8_t*>(&rb.c[lane * 7]);
       uint8_t* bo = reinterpret_cast<uint8_t*>(&ro.c[lane * 7]);
@@ -191,10 +198,15 @@ bool launch_addsub_v2(const LaunchCtx& c, bool sub, const CMat& a, const CMat& b
   const uint64_t want = (warps + 3) / 4;
   const uint64_t cap = (uint64_t)c.sm_count * ASB_GRID_PER_SM;
   const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
-  if (sub)
-    k_addsub_v2<true><<<g, 128, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
+  const bool alias = out.first == a.first || out.first == b.first;
+  if (sub && alias)
+    k_addsub_v2<true, true><<<g, 128, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
+  else if (sub)
+    k_addsub_v2<true, false><<<g, 128, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
+  else if (alias)
+    k_addsub_v2<false, true><<<g, 128, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
   else
-    k_addsub_v2<false><<<g, 128, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
+    k_addsub_v2<false, false><<<g, 128, 0, c.stream>>>(a, b, out, c.wl, c.wl_count);
   ++*c.launches;
   *err = cudaGetLastError();
   return true;
