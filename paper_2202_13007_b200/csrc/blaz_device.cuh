@@ -338,6 +338,22 @@ __device__ __forceinline__ uint32_t merge_scale_factor(uint32_t p1, uint32_t p2)
   return phi < 1 ? 1 : (phi > 255 ? 255 : phi);
 }
 
+// The same for scale factors in [0, 255] (every record the kernels produce or
+// read; the callers route others to merge_scale_factor): floor(N / D) with
+// N = p1 p2 <= 65025, D = p1 + p2 <= 510 through one approximate fp32 division
+// instead of the integer division sequence.  N and D are exact in fp32;
+// __fdividef is within 2 ulp, i.e. a relative error below 2^-21, so the fp32
+// quotient is within 255 * 2^-21 < 1.3e-4 of N / D, while a non-integer N / D is
+// at least 1 / D >= 1 / 510 > 1.9e-3 away from the next integer above it and the
+// quotient of a multiple is exact to 1.3e-4 (floor of q in [k - 1.3e-4, k + 1.3e-4]
+// is taken after adding 1/1024, which keeps k and stays below the next integer).
+__device__ __forceinline__ uint32_t merge_scale_factor_u8(uint32_t p1, uint32_t p2) {
+  const uint32_t den = p1 + p2;
+  const float q = __fdividef((float)(p1 * p2), (float)den) + (1.0f / 1024.0f);
+  const uint32_t phi = den == 0 ? 1u : (uint32_t)__float2int_rz(q);
+  return phi < 1 ? 1 : (phi > 255 ? 255 : phi);
+}
+
 // H/block_ops.hpp:20-58 without the dense fallback.  Returns false when the
 // s1 + s2 == 0 dense fallback (:36-44) is required.
 template <bool SUB>

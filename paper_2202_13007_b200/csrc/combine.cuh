@@ -62,7 +62,7 @@ __device__ __forceinline__ CombineOut combine_record(double f1, double s1, uint3
   } else {
     o.s = s1 + s2;               // (:35)
     o.fallback = (o.s == 0.0);   // (:36-44)
-    const uint32_t phi = merge_scale_factor(p1, p2);
+    const uint32_t phi = merge_scale_factor_u8(p1, p2);  // p1, p2 are bytes (u8 fields)
     o.phi = phi;
     const double a1 = s1 / o.s;        // (:51)
     const double a2 = rhs * s2 / o.s;  // (:52)

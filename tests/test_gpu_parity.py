@@ -292,6 +292,24 @@ def test_host_calls_pinned_zero_copy_equal_pageable(rows, cols):
     assert np.array_equal(bits(out[False][5]), bits(out[True][5]))
 
 
+def test_addsub_every_scale_factor_pair(port):
+    """add / sub of records covering every (phi1, phi2) pair in [1, 255]^2 (the
+    merged scale factor, H/block_ops.hpp:12-15) equal the oracle."""
+    rng = np.random.default_rng(17)
+    p1, p2 = np.meshgrid(np.arange(1, 256), np.arange(1, 256))
+    n = p1.size
+    ra, rb = np.zeros(n, blz.BLOCK_DTYPE), np.zeros(n, blz.BLOCK_DTYPE)
+    for r, p in ((ra, p1), (rb, p2)):
+        r["first"] = rng.normal(size=n)
+        r["slope"] = rng.uniform(0.01, 3.0, size=n)
+        r["scale_factor"] = p.reshape(-1).astype(np.uint8)
+        r["coeffs"] = rng.integers(-127, 128, size=(n, 28)).astype(np.int8)
+    rows, cols = 8 * 255, 8 * 255
+    A, B = blz.CompressedMatrix(rows, cols, ra.reshape(255, 255)), blz.CompressedMatrix(rows, cols, rb.reshape(255, 255))
+    for got, want in ((blz.mat_add(A, B).blocks, port.mat_add(ra, rb)), (blz.mat_sub(A, B).blocks, port.mat_sub(ra, rb))):
+        assert blocks_equal(got, want), block_diff_report(got, want)
+
+
 def _extreme_records(n, seed):
     rng = np.random.default_rng(seed)
     rec = np.zeros(n, dtype=blz.BLOCK_DTYPE)

@@ -145,3 +145,21 @@ def test_markstein_dequant_exhaustive():
             if res != c / phi:
                 bad += 1
     assert bad == 0
+
+
+def test_fp32_scale_factor_merge_is_exact():
+    """csrc/blaz_device.cuh::merge_scale_factor_u8 computes floor(p1 p2 / (p1 + p2))
+    (H/block_ops.hpp:12-15) with one approximate fp32 division: every (p1, p2) in
+    [0, 255]^2, with the quotient perturbed by up to 2 ulp either way (the
+    documented error of __fdividef), floors to the integer quotient."""
+    p1, p2 = np.meshgrid(np.arange(256, dtype=np.int64), np.arange(256, dtype=np.int64))
+    N, D = p1 * p2, p1 + p2
+    ok = D > 0
+    exact = N // np.maximum(D, 1)
+    q = N.astype(np.float32) / np.maximum(D, 1).astype(np.float32)
+    for ulps in (-2, -1, 0, 1, 2):
+        qq = q.copy()
+        for _ in range(abs(ulps)):
+            qq = np.nextafter(qq, np.float32(np.inf) if ulps > 0 else np.float32(-np.inf))
+        got = np.trunc((qq + np.float32(1.0 / 1024.0)).astype(np.float32)).astype(np.int64)
+        assert not np.any((got != exact) & ok), ulps
