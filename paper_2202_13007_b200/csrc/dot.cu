@@ -186,39 +186,40 @@ __global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a,
 }
 
 // Ascending serial sum from +0.0 (the restated oracle's order; inherently one
-// dependent DADD chain).  One warp: lanes load 32 consecutive values per step
-// (coalesced, several steps in flight), lane 0 adds them in order from
-// registers via shuffles, so the chain runs at the DADD latency instead of the
-// load latency.
+// dependent DADD chain).  One thread: the next 32 values are loaded (16-byte
+// loads when aligned) while the current 32 are added, so the chain runs at the
+// DADD latency rather than the load latency.
 __global__ void __launch_bounds__(32) k_sum(const double* __restrict__ v, uint64_t n, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
+  if (threadIdx.x != 0) return;
   double s = 0.0;
-  constexpr int AHEAD = 8;
-  double buf[AHEAD];
-  const uint64_t steps = (n + 31) / 32;
+  constexpr int G = 32;
+  const uint64_t full = (reinterpret_cast<uintptr_t>(v) & 15) == 0 ? n / G : 0;
+  double cur[G], nxt[G];
+  if (full) {
 #pragma unroll
-  for (int k = 0; k < AHEAD; ++k) {
-    const uint64_t i = (uint64_t)k * 32 + lane;
-    buf[k] = i < n ? v[i] : 0.0;
-  }
-  for (uint64_t st = 0; st < steps; st += AHEAD) {
-#pragma unroll
-    for (int k = 0; k < AHEAD; ++k) {
-      const double x = buf[k];
-      const uint64_t nx = (st + k + AHEAD) * 32 + lane;
-      buf[k] = nx < n ? v[nx] : 0.0;
-      const uint64_t base = (st + k) * 32;
-      if (base < n) {
-        const int cnt = n - base < 32 ? (int)(n - base) : 32;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const double y = __shfl_sync(0xffffffffu, x, q);
-          if (q < cnt) s += y;
-        }
-      }
+    for (int k = 0; k < G / 2; ++k) {
+      const double2 p = reinterpret_cast<const double2*>(v)[k];
+      cur[2 * k] = p.x;
+      cur[2 * k + 1] = p.y;
     }
   }
-  if (lane == 0) *out = s;
+  for (uint64_t g = 0; g < full; ++g) {
+    if (g + 1 < full) {
+      const double2* src = reinterpret_cast<const double2*>(v + (g + 1) * G);
+#pragma unroll
+      for (int k = 0; k < G / 2; ++k) {
+        const double2 p = src[k];
+        nxt[2 * k] = p.x;
+        nxt[2 * k + 1] = p.y;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < G; ++k) s += cur[k];
+#pragma unroll
+    for (int k = 0; k < G; ++k) cur[k] = nxt[k];
+  }
+  for (uint64_t k = full * G; k < n; ++k) s += v[k];
+  *out = s;
 }
 
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
