@@ -17,7 +17,7 @@ for r in csv.DictReader(lines):
     if r.get("Metric Name") != "gpu__time_duration.sum":
         continue
     name = r["Kernel Name"]
-    if "blz::" not in name:
+    if "blz::" not in name and not re.match(r"^(void )?k_", name):
         continue
     short = re.sub(r"^void ", "", name)
     short = re.sub(r"blz::(<unnamed>::)?", "", short)
