@@ -169,6 +169,16 @@ blz_status blz_matmul_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, in
                           void* scratch, const blz_cmat* out);
 blz_status blz_matmul_dense_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, int mode,
                                 void* scratch, double* out, uint64_t ld);
+/* K-paneled variants (HBM capacity): B is decompressed
+ * panel_block_rows block-rows at a time (a positive multiple of 4) and each
+ * panel's product accumulated into C; bitwise the results of the one-pass calls.
+ * scratch: blz_matmul_panel_scratch_bytes(a, b, panel_block_rows) bytes (dense A,
+ * one B panel and, for the compressed output, dense C). */
+uint64_t blz_matmul_panel_scratch_bytes(const blz_cmat* a, const blz_cmat* b, uint64_t panel_block_rows);
+blz_status blz_matmul_panel_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, int mode,
+                                uint64_t panel_block_rows, void* scratch, const blz_cmat* out);
+blz_status blz_matmul_dense_panel_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, int mode,
+                                      uint64_t panel_block_rows, void* scratch, double* out, uint64_t ld);
 /* ---- block-row sharded operations over NCCL --------
  * `nccl_comm` is an ncclComm_t of G ranks (one GPU each); rank r owns
  * block-rows [BR*r/G, BR*(r+1)/G) of every operand and result.  NCCL is

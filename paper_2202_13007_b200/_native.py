@@ -82,6 +82,11 @@ SIGNATURES = {
     "blz_sub_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),
     "blz_scale_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
     "blz_scale_meta_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat)]),
+    "blz_matmul_panel_scratch_bytes": (_U64, [C.POINTER(blz_cmat), C.POINTER(blz_cmat), _U64]),
+    "blz_matmul_panel_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.c_int, _U64, _P,
+                                   C.POINTER(blz_cmat)]),
+    "blz_matmul_dense_panel_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.c_int, _U64, _P, _P,
+                                         _U64]),
     "blz_reconstruct_rows_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_int, _P]),
     "blz_reconstruct_cols_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_int, _P]),
     "blz_block_mul_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P]),

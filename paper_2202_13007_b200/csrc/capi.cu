@@ -666,6 +666,80 @@ blz_status blz_matmul_dense_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b
   return BLZ_OK;
 }
 
+// ---- K-paneled compressed GEMM (decompression fed to the GEMM
+// panel by panel, for HBM capacity) -------------------------------------------
+// B is decompressed P block-rows at a time (a contiguous block-row range of its
+// SoA arrays) and each panel's product is accumulated into C, the accumulators
+// continuing from the previous panels' values: per output entry the operation
+// sequence is exactly the single-pass one (H/matrix.hpp:188-202), so results are
+// bitwise those of blz_matmul_dev.  Scratch: dense A + one B panel + dense C
+// instead of dense A + dense B + dense C (8 GiB instead of 15 GiB per rank for
+// config 4 on 8 GPUs, with 1/8 panels).
+uint64_t blz_matmul_panel_scratch_bytes(const blz_cmat* a, const blz_cmat* b, uint64_t panel_block_rows) {
+  if (!a || !b || panel_block_rows == 0) return 0;
+  const uint64_t ma = 8 * a->block_rows, ka = 8 * a->block_cols, nn = 8 * b->block_cols;
+  const uint64_t pr = std::min<uint64_t>(panel_block_rows, b->block_rows);
+  return (ma * ka + 8 * pr * nn + ma * nn) * sizeof(double) + 256;
+}
+
+}  // extern "C"
+namespace {
+blz_cmat sub_rows(const blz_cmat& m, uint64_t b0, uint64_t b1);
+}
+extern "C" {
+
+static blz_status matmul_panel_common(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int mode,
+                                      uint64_t panel_block_rows, void* scratch, double* dc, uint64_t ldc,
+                                      uint64_t crop_m, uint64_t crop_n) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "mat_mul")) return st;
+  if (blz_status st = check_cmat(c, b, "mat_mul")) return st;
+  if (a->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: inner dimension mismatch");  // :207
+  if (mode < BLZ_GEMM_EXACT || mode > BLZ_GEMM_FUSED_DFMA) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: bad mode");
+  if (!scratch) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: null scratch");
+  if (panel_block_rows == 0 || panel_block_rows % 4)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: panel_block_rows must be a positive multiple of 4");
+  const uint64_t ma = 8 * a->block_rows, ka = 8 * a->block_cols, nn = 8 * b->block_cols;
+  double* da = (double*)scratch;
+  double* db = da + ma * ka;
+  if (!dc) dc = db + 8 * std::min<uint64_t>(panel_block_rows, b->block_rows) * nn;
+  auto L = lc(c);
+  BLZ_CUDA(c, blz::launch_decompress(L, c->basis, view(a), da, ka, ma, ka), "mat_mul decompress A");
+  for (uint64_t p0 = 0; p0 < b->block_rows; p0 += panel_block_rows) {
+    const uint64_t p1 = std::min(b->block_rows, p0 + panel_block_rows);
+    const uint64_t k0 = 8 * p0, k1 = std::min<uint64_t>(8 * p1, a->cols);
+    if (k1 <= k0) break;
+    const blz_cmat bp = sub_rows(*b, p0, p1);
+    BLZ_CUDA(c, blz::launch_decompress(L, c->basis, view(&bp), db, nn, 8 * (p1 - p0), nn), "mat_mul decompress B");
+    BLZ_CUDA(c, blz::launch_gemm(L, mode, da + k0, ka, db, nn, dc, ldc, crop_m, crop_n, k1 - k0, p0 > 0),
+             "mat_mul gemm");
+  }
+  return BLZ_OK;
+}
+
+blz_status blz_matmul_panel_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int mode, uint64_t panel_block_rows,
+                                void* scratch, const blz_cmat* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, out, "mat_mul")) return st;
+  if (out->rows != a->rows || out->cols != b->cols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: output dimension mismatch");
+  const uint64_t ma = 8 * a->block_rows, nn = 8 * b->block_cols;
+  double* dc = (double*)scratch + ma * 8 * a->block_cols +
+               8 * std::min<uint64_t>(panel_block_rows ? panel_block_rows : 1, b->block_rows) * nn;
+  // full accumulator tiles (padding included), each compressed once (H/matrix.hpp:231-233)
+  if (blz_status st = matmul_panel_common(c, a, b, mode, panel_block_rows, scratch, dc, nn, ma, nn)) return st;
+  if (blz_status st = ensure_worklist(c, a->block_rows * b->block_cols)) return st;
+  return cuda_err(c, blz::launch_compress(lc(c), c->basis, dc, ma, nn, nn, view(out)), "mat_mul compress");
+}
+
+blz_status blz_matmul_dense_panel_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int mode,
+                                      uint64_t panel_block_rows, void* scratch, double* out, uint64_t ld) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (a && b && ld < b->cols) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul_dense: ld < cols");
+  // crop (H/matrix.hpp:242-248): the panels accumulate straight into the caller's a.rows x b.cols
+  return matmul_panel_common(c, a, b, mode, panel_block_rows, scratch, out, ld, a ? a->rows : 0, b ? b->cols : 0);
+}
+
 blz_status blz_pack_aos_dev(blz_ctx* c, const blz_cmat* in, blz_block* out) {
   if (!c) return BLZ_INVALID_ARGUMENT;
   if (blz_status st = check_cmat(c, in, "pack")) return st;

@@ -36,11 +36,14 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 
 // FMA = false: acc + a*b as DMUL then DADD (-fmad=false); true: one DFMA.
+// ACC: the accumulators start from C (a K-panel continuing the chain of the
+// previous panels: storing and reloading a double is exact, so the per-entry
+// operation sequence is the single-pass one); otherwise from +0.0.
 template <bool FMA>
 __global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A, uint64_t lda,
                                                     const double* __restrict__ Bm, uint64_t ldb,
                                                     double* __restrict__ Cm, uint64_t ldc, uint64_t M,
-                                                    uint64_t N, uint64_t K) {
+                                                    uint64_t N, uint64_t K, bool acc_c) {
   extern __shared__ __align__(16) double esm[];
   double* As0 = esm;                      // [2][EBM * EAS]
   double* Bs0 = esm + 2 * EBM * EAS;      // [2][EBK * EBN]
@@ -88,7 +91,10 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A,
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t gr = m0 + ty * 8 + i, gc = n0 + (j / 2) * 32 + 2 * tx + (j % 2);
+      acc[i][j] = (acc_c && gr < M && gc < N) ? Cm[gr * ldc + gc] : 0.0;
+    }
 
   const uint64_t ntiles = (K + EBK - 1) / EBK;
   load_tile(0, 0);
@@ -155,7 +161,7 @@ constexpr int DBS = DBN + 4;   // Bs[k][n] row stride = 4 mod 16 doubles
 __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A, uint64_t lda,
                                                    const double* __restrict__ Bm, uint64_t ldb,
                                                    double* __restrict__ Cm, uint64_t ldc, uint64_t M,
-                                                   uint64_t N, uint64_t K) {
+                                                   uint64_t N, uint64_t K, bool acc_c) {
   extern __shared__ __align__(16) double dsm[];
   double* As0 = dsm;
   double* Bs0 = dsm + 2 * DBM * DAS;
@@ -203,7 +209,12 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < 4; ++j) {  // D fragment: row = lane>>2, cols = (lane&3)*2 + {0,1}
+      const uint64_t gr = m0 + wm * 64 + i * 8 + (lane >> 2);
+      const uint64_t gc = n0 + wn * 32 + j * 8 + (lane & 3) * 2;
+      acc[i][j][0] = (acc_c && gr < M && gc < N) ? Cm[gr * ldc + gc] : 0.0;
+      acc[i][j][1] = (acc_c && gr < M && gc + 1 < N) ? Cm[gr * ldc + gc + 1] : 0.0;
+    }
 
   const uint64_t ntiles = (K + DBK - 1) / DBK;
   load_tile(0, 0);
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
 #endif
 
 cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t lda, const double* Bm,
-                        uint64_t ldb, double* Cm, uint64_t ldc, uint64_t M, uint64_t N, uint64_t K) {
+                        uint64_t ldb, double* Cm, uint64_t ldc, uint64_t M, uint64_t N, uint64_t K, bool acc_c) {
   if (mode == 1) mode = FUSED_KERNEL_DEFAULT;
   // per call: the smem attribute belongs to the current device (a few microseconds
   // against a GEMM of milliseconds)
@@ -265,14 +276,14 @@ cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t 
     const size_t smem = (size_t)(2 * DBM * DAS + 2 * DBK * DBS) * sizeof(double);
     cudaError_t ea = cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return ea;
-    k_gemm_dmma<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
+    k_gemm_dmma<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K, acc_c);
   } else {
     dim3 grid((unsigned)((N + EBN - 1) / EBN), (unsigned)((M + EBM - 1) / EBM));
     const size_t smem = (size_t)(2 * EBM * EAS + 2 * EBK * EBN) * sizeof(double);
     auto kern = mode == 3 ? k_gemm_simt<true> : k_gemm_simt<false>;
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return ea;
-    kern<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K);
+    kern<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K, acc_c);
   }
   ++*c.launches;
   return cudaGetLastError();

@@ -78,6 +78,7 @@ cudaError_t launch_mean_rel_error(const LaunchCtx& c, const double* ref, const d
                                   double* mean, unsigned long long* excluded);
 // gemm.cu
 cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t lda, const double* Bm,
-                        uint64_t ldb, double* Cm, uint64_t ldc, uint64_t M, uint64_t N, uint64_t K);
+                        uint64_t ldb, double* Cm, uint64_t ldc, uint64_t M, uint64_t N, uint64_t K,
+                        bool acc_c = false);
 
 }  // namespace blz

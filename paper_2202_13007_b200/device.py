@@ -328,5 +328,32 @@ def matmul_dense(a: DeviceCMat, b: DeviceCMat, mode: int = N.GEMM_EXACT, out: to
     return out
 
 
+def matmul_panel_scratch(a: DeviceCMat, b: DeviceCMat, panel_block_rows: int) -> torch.Tensor:
+    n = int(N.load().blz_matmul_panel_scratch_bytes(a.ref(), b.ref(), int(panel_block_rows)))
+    return torch.empty(n, dtype=torch.uint8, device=a.buf.device)
+
+
+def matmul_panel(a: DeviceCMat, b: DeviceCMat, panel_block_rows: int, mode: int = N.GEMM_EXACT,
+                 out: DeviceCMat | None = None, scratch: torch.Tensor | None = None) -> DeviceCMat:
+    """mat_mul with B decompressed panel_block_rows block-rows at a time (bitwise = matmul)."""
+    ctx = context(a.buf.device.index)
+    scratch = scratch if scratch is not None else matmul_panel_scratch(a, b, panel_block_rows)
+    out = out or DeviceCMat(a.rows, b.cols, device=a.buf.device)
+    ctx.check(ctx.lib.blz_matmul_panel_dev(ctx.handle, a.ref(), b.ref(), mode, int(panel_block_rows),
+                                           _ptr(scratch), out.ref()))
+    return out
+
+
+def matmul_dense_panel(a: DeviceCMat, b: DeviceCMat, panel_block_rows: int, mode: int = N.GEMM_EXACT,
+                       out: torch.Tensor | None = None, scratch: torch.Tensor | None = None) -> torch.Tensor:
+    ctx = context(a.buf.device.index)
+    scratch = scratch if scratch is not None else matmul_panel_scratch(a, b, panel_block_rows)
+    if out is None:
+        out = torch.empty((a.rows, b.cols), dtype=torch.float64, device=a.buf.device)
+    ctx.check(ctx.lib.blz_matmul_dense_panel_dev(ctx.handle, a.ref(), b.ref(), mode, int(panel_block_rows),
+                                                 _ptr(scratch), _ptr(out), out.stride(0)))
+    return out
+
+
 def sync(device: int | None = None):
     context(device).sync()

@@ -577,6 +577,29 @@ def test_matmul_fused_kernels_bitwise_equal(shape):
         dev.matmul_dense(A, B, mode=7)
 
 
+@pytest.mark.parametrize("mode", [blz.GEMM_EXACT, blz.GEMM_FUSED])
+@pytest.mark.parametrize("shape,panel", [((200, 333, 136), 4), ((64, 1000, 72), 8), ((40, 96, 48), 12)])
+def test_matmul_panels_bitwise_equal_one_pass(shape, panel, mode, port):
+    """K-paneled matmul (B decompressed panel by panel, accumulators continued) equals
+    the one-pass product bitwise, compressed and dense, ragged K included; exact mode
+    also equals the oracle."""
+    m, k, n = shape
+    A = dev.compress(W.smooth_field(m, k, seed=47, device="cuda"))
+    B = dev.compress(W.rough_uniform(k, n, seed=48, device="cuda"))
+    one = dev.matmul(A, B, mode=mode)
+    pan = dev.matmul_panel(A, B, panel, mode=mode)
+    d1 = dev.matmul_dense(A, B, mode=mode)
+    d2 = dev.matmul_dense_panel(A, B, panel, mode=mode)
+    dev.sync()
+    assert _equal_cmats(one, pan)
+    assert torch.equal(d1.view(torch.int64), d2.view(torch.int64))
+    if mode == blz.GEMM_EXACT:
+        want = port.mat_mul(A.to_host().blocks, m, k, B.to_host().blocks, k, n)
+        assert blocks_equal(pan.to_host().blocks, want)
+    with pytest.raises(blz.InvalidArgument, match="multiple of 4"):
+        dev.matmul_panel(A, B, 3, mode=mode)
+
+
 # ---- .blzc container (SURVEY.md 8f-1; H/io.hpp:93-134) --------------------------
 @pytest.mark.parametrize("n", range(10))
 def test_blzc_bytes_match_reference(golden, n):

@@ -40,3 +40,26 @@ for mode in (int(m) for m in a.modes.split(",")):
 dev.sync()
 torch.cuda.synchronize()
 print("ok")
+
+# K-paneled variant (B decompressed panel by panel) against the one-pass call
+if a.time:
+    for panel in (a.n // 8 // 8, a.n // 8 // 2):
+        scr = dev.matmul_panel_scratch(A, B, panel)
+        dev.matmul_panel(A, B, panel, mode=1, out=C, scratch=scr)
+        dev.sync()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        for _ in range(a.reps):
+            dev.matmul_panel(A, B, panel, mode=1, out=C, scratch=scr)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / a.reps
+        print(f"fused, B in panels of {panel} block-rows: matmul {a.n}^3 {ms:.3f} ms, scratch {scr.numel() / 2**30:.2f} GiB "
+              f"(one pass: {scratch.numel() / 2**30:.2f} GiB)", flush=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(a.reps):
+        dev.matmul(A, B, mode=1, out=C, scratch=scratch)
+    ev[1].record()
+    torch.cuda.synchronize()
+    print(f"fused, one pass: matmul {a.n}^3 {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms", flush=True)
