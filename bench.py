@@ -309,6 +309,7 @@ def run_ours(args, cfg, rank, world, local):
     s1, s2, s3 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
 
     def step_dag():
+        stream = torch.cuda.current_stream()  # the capture stream while a CUDA graph records
         dev.compress(A, cA)
         ea = torch.cuda.Event()
         ea.record(stream)
@@ -339,6 +340,24 @@ def run_ours(args, cfg, rank, world, local):
     def all_launches():
         return sum(c.launches() for c in dev.contexts(local))
 
+    # The op graph captured once as a CUDA graph and replayed: one launch per step
+    # from the host, the kernels' dependencies resolved on the device.
+    graph_launches = None
+    if args.graph and not args.sequential:
+        cap = torch.cuda.Stream()
+        with torch.cuda.stream(cap):  # warm the capture stream's context (scratch, worklists) outside capture
+            step_dag()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        l_cap = all_launches()
+        with torch.cuda.graph(g, stream=cap):
+            step_dag()
+        graph_launches = all_launches() - l_cap
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        timed_step = g.replay
+
     # timed region: K steps on the launching stream (the DAG joins back into it)
     l0 = all_launches()
     with ClockSampler(local) as clk:
@@ -353,6 +372,8 @@ def run_ours(args, cfg, rank, world, local):
         torch.cuda.synchronize()
         barrier(world)
     launches = all_launches() - l0
+    if graph_launches is not None:  # replays do not pass through the host launch counter
+        launches = graph_launches * args.steps
     ctx.sync()
     ms_local = start.elapsed_time(end) / args.steps
     ms = max_over_ranks(ms_local, world)
@@ -400,7 +421,8 @@ def run_ours(args, cfg, rank, world, local):
                        "mode": "bit-exact: verified fast compress + reference-order kernels (-fmad=false)",
                        "schedule": ("one stream, op order" if args.sequential else
                                     "op graph on 3 streams (scale+decompress overlaps compress(B); "
-                                    "add+decompress || sub+decompress)"),
+                                    "add+decompress || sub+decompress)"
+                                    + (", captured once as a CUDA graph and replayed" if args.graph else "")),
                        "ops_timing": "per-op ms from a separate sequential pass (CUDA events between ops)"},
             "ops": op_report,
             "roofline": {"bound": "hbm", "kernel": "k_decompress", "achieved": dec["gbs"], "peak": hbm,
@@ -909,6 +931,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
     ap.add_argument("--sequential", action="store_true", help="time the one-stream op order instead of the DAG")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="issue the op graph from the host each step instead of replaying a captured CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -600,6 +600,40 @@ def test_matmul_panels_bitwise_equal_one_pass(shape, panel, mode, port):
         dev.matmul_panel(A, B, 3, mode=mode)
 
 
+def test_device_calls_capture_into_cuda_graph():
+    """The device API is stream-ordered and allocation-free after the first call, so a
+    config-1-style op chain captures into a CUDA graph; replays equal eager calls."""
+    rows, cols = 520, 776
+    a = W.quadratic_blocks(rows, cols, seed=93, device="cuda")
+    b = W.quadratic_blocks(rows, cols, seed=94, device="cuda")
+    cA, cB, cS = dev.DeviceCMat(rows, cols), dev.DeviceCMat(rows, cols), dev.DeviceCMat(rows, cols)
+    cK = dev.ScaledCMat(cA)
+    oS, oK = torch.empty_like(a), torch.empty_like(a)
+
+    def chain():
+        dev.compress(a, cA)
+        dev.compress(b, cB)
+        dev.sub(cA, cB, cS)
+        dev.scale_meta(cA, -2.5, cK)
+        dev.decompress(cS, oS)
+        dev.decompress(cK, oK)
+
+    cap = torch.cuda.Stream()
+    with torch.cuda.stream(cap):
+        chain()
+    torch.cuda.synchronize()
+    want = [x.clone() for x in (cA.buf, cB.buf, cS.buf, cK.buf, oS, oK)]
+    for x in (cA.buf, cB.buf, cS.buf, cK.buf, oS, oK):
+        x.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        chain()
+    g.replay()
+    torch.cuda.synchronize()
+    for x, y in zip((cA.buf, cB.buf, cS.buf, cK.buf, oS, oK), want):
+        assert torch.equal(x.view(torch.uint8), y.view(torch.uint8))
+
+
 # ---- .blzc container (SURVEY.md 8f-1; H/io.hpp:93-134) --------------------------
 @pytest.mark.parametrize("n", range(10))
 def test_blzc_bytes_match_reference(golden, n):
