@@ -70,7 +70,7 @@ struct blz_ctx {
 
 namespace {
 
-enum SlotId { S_UNUSED = 0, S_IN0, S_IN1, S_OUT, S_CM0, S_CM1, S_CM2, S_AUX };
+enum SlotId { S_ROWDOT = 0, S_IN0, S_IN1, S_OUT, S_CM0, S_CM1, S_CM2, S_AUX };
 
 blz_status set_err(blz_ctx* c, blz_status st, const std::string& msg) {
   if (c) c->err = msg;
@@ -599,7 +599,10 @@ blz_status blz_rowdot_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, doub
   if (blz_status st = check_cmat(c, b, "mat_rowdot")) return st;
   if (blz_status st = same_dims(c, a->rows, a->cols, b->rows, b->cols, "mat_rowdot")) return st;
   if (a->block_rows * a->block_cols == 0) return BLZ_OK;
-  return cuda_err(c, blz::launch_rowdot(lc(c), c->basis, view(a), view(b), r), "mat_rowdot");
+  cudaError_t e;
+  void* scratch = slot(c, S_ROWDOT, blz::rowdot_scratch_bytes(view(a)), &e);  // grow-only context scratch
+  if (!scratch) return cuda_err(c, e, "scratch allocation");
+  return cuda_err(c, blz::launch_rowdot(lc(c), c->basis, view(a), view(b), r, scratch), "mat_rowdot");
 }
 
 blz_status blz_sum_dev(blz_ctx* c, const double* v, uint64_t n, double* out) {

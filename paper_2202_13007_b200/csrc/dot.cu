@@ -12,6 +12,8 @@
 #include "blaz_device.cuh"
 #include "launch.h"
 
+#include <algorithm>
+
 namespace blz {
 
 template <bool SYM>
@@ -125,10 +127,13 @@ __global__ void __launch_bounds__(128) k_dot_warp(const Basis B, CMat a, CMat b,
 // operation sequence as the single-threaded restatement.  Row stride 9 and
 // slot stride 74 doubles keep the chain reads bank-conflict-free.
 constexpr int RD_WARPS = 2;
+#ifndef RD_MINB
+#define RD_MINB 1
+#endif
 constexpr int RD_SLOT = 74;
 
 template <bool SYM>
-__global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a, CMat b, double* __restrict__ r) {
+__global__ void __launch_bounds__(RD_WARPS * 32, RD_MINB) k_rowdot(const Basis B, CMat a, CMat b, double* __restrict__ r) {
   __shared__ double P[RD_WARPS][32 * RD_SLOT];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* S = P[warp];
@@ -183,6 +188,105 @@ __global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a,
     const uint64_t row = crow * BD + u_own;
     if (crow < a.br && row < a.rows) r[row] = acc;
   }
+}
+
+// The same row dots as a persistent kernel over split work items: a group's
+// block-columns are cut into RD_SPLIT consecutive ranges, and item (q, g) advances
+// group g's 32 row chains over range q, starting from the accumulators item
+// (q-1, g) left in global memory (storing and reloading a double is exact, so
+// every chain is the same single operation sequence).  Items are claimed in
+// order from an atomic counter -- all first ranges, then all second ranges, ... --
+// so an item's predecessor was claimed earlier by a running warp and the wait
+// for it is short; finer items fill the last wave of resident warps (2,048
+// groups at 65536^2 are 1.73 waves of the 1,184 resident warps; 8,192 quarter
+// items are 6.9 waves).
+#ifndef RD_SPLIT
+#define RD_SPLIT 16  // 65536^2: 21.2 ms unsplit, 16.7 / 16.4 / 16.5 ms with 8 / 16 / 32 ranges
+#endif
+
+template <bool SYM>
+__global__ void __launch_bounds__(RD_WARPS * 32, RD_MINB)
+    k_rowdot_split(const Basis B, CMat a, CMat b, double* __restrict__ r, unsigned long long* __restrict__ counter,
+                   int* __restrict__ flags, double* __restrict__ state, int nsplit) {
+  __shared__ double P[RD_WARPS][32 * RD_SLOT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* S = P[warp];
+  const uint64_t groups = (a.br + 3) / 4;
+  const uint64_t items = groups * nsplit;
+  const bool is_b = lane >= 16;
+  const int dl = lane & 15;
+  const int dgrp = dl >> 2, dcol = dl & 3;
+  const int cgrp = lane >> 3, u_own = lane & 7;
+  for (;;) {
+    unsigned long long w = 0;
+    if (lane == 0) w = atomicAdd(counter, 1ull);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    if (w >= items) break;
+    const int q = (int)(w / groups);
+    const uint64_t g = w % groups;
+    // block-column range of item q: cut points at multiples of 4 (one chunk)
+    const uint64_t c0 = (a.bc * (uint64_t)q / nsplit) / 4 * 4;
+    const uint64_t c1 = q == nsplit - 1 ? a.bc : (a.bc * (uint64_t)(q + 1) / nsplit) / 4 * 4;
+    const uint64_t drow = g * 4 + dgrp, crow = g * 4 + cgrp;
+    double acc = 0.0;
+    if (q > 0) {  // wait for item (q-1, g), then continue its chains
+      if (lane == 0) {
+        while (*(volatile int*)(flags + g) < q) __nanosleep(200);
+      }
+      __syncwarp();
+      __threadfence();
+      acc = __ldcg(state + g * 32 + lane);
+    }
+    for (uint64_t t0 = c0; t0 < c1; t0 += 4) {
+      {
+        const uint64_t t = min(t0 + dcol, a.bc - 1), dr = min(drow, a.br - 1);
+        const uint64_t idx = dr * a.bc + t;
+        RBlock blk;
+        blk.f = is_b ? b.first[idx] : a.first[idx];
+        blk.s = is_b ? b.slope[idx] : a.slope[idx];
+        blk.phi = is_b ? b.scale[idx] : a.scale[idx];
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>((is_b ? b.coeffs : a.coeffs) + idx * KEPT);
+#pragma unroll
+        for (int w2 = 0; w2 < 7; ++w2) blk.c[w2] = cw[w2];
+        double* slot = S + lane * RD_SLOT;
+        decompress_exact<SYM>(blk, B, [&](int u, const double (&row)[BD]) {
+#pragma unroll
+          for (int v = 0; v < BD; ++v) slot[u * 9 + v] = row[v];
+        });
+      }
+      __syncwarp();
+      if (crow < a.br) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t tk = t0 + k;
+          if (tk < c1) {
+            const uint64_t rem = a.cols - tk * BD;
+            const int jlim = rem < BD ? (int)rem : BD;
+            const double* sa = S + (cgrp * 4 + k) * RD_SLOT + u_own * 9;
+            const double* sb = S + (16 + cgrp * 4 + k) * RD_SLOT + u_own * 9;
+#pragma unroll
+            for (int v = 0; v < BD; ++v)
+              if (v < jlim) acc += sa[v] * sb[v];
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (q == nsplit - 1) {
+      const uint64_t row = crow * BD + u_own;
+      if (crow < a.br && row < a.rows) r[row] = acc;
+    } else {
+      __stcg(state + g * 32 + lane, acc);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicExch(flags + g, q + 1);
+    }
+  }
+}
+
+uint64_t rowdot_scratch_bytes(const CMat& a) {
+  const uint64_t groups = (a.br + 3) / 4;
+  return 256 + groups * 4 + 256 + groups * 32 * sizeof(double);
 }
 
 // Ascending serial sum from +0.0 (the restated oracle's order; inherently one
@@ -245,8 +349,32 @@ cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a
   return cudaGetLastError();
 }
 
-cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r) {
+cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r,
+                          void* scratch) {
   const uint64_t groups = (a.br + 3) / 4;
+  const bool sym = c.basis_sym && !c.exact_only;
+  // at least 8 chunks of 4 block-columns per range
+  const int nsplit = (int)std::max<uint64_t>(1, std::min<uint64_t>(RD_SPLIT, a.bc / 32));
+  if (scratch && nsplit > 1) {
+    unsigned long long* counter = (unsigned long long*)scratch;
+    int* flags = (int*)((char*)scratch + 256);
+    double* state = (double*)((char*)scratch + 256 + ((groups * 4 + 255) / 256) * 256);
+    cudaError_t e = cudaMemsetAsync(scratch, 0, 256 + groups * 4, c.stream);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = sym ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowdot_split<true>, RD_WARPS * 32, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowdot_split<false>, RD_WARPS * 32, 0);
+    if (e != cudaSuccess) return e;
+    const uint64_t want = (groups * nsplit + RD_WARPS - 1) / RD_WARPS;
+    const uint64_t cap = (uint64_t)c.sm_count * (per_sm > 0 ? per_sm : 1);
+    const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    if (sym)
+      k_rowdot_split<true><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r, counter, flags, state, nsplit);
+    else
+      k_rowdot_split<false><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r, counter, flags, state, nsplit);
+    ++*c.launches;
+    return cudaGetLastError();
+  }
   const uint64_t want = (groups + RD_WARPS - 1) / RD_WARPS;
   const uint64_t cap = (uint64_t)c.sm_count * 16;
   const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);

@@ -66,7 +66,10 @@ cudaError_t launch_unpack_blzc(const LaunchCtx& c, const uint8_t* in, const CMat
 // dot.cu
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out);
-cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r);
+cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r,
+                          void* scratch = nullptr);
+// scratch for the split persistent row-dot kernel (counter, flags, chain state)
+uint64_t rowdot_scratch_bytes(const CMat& a);
 cudaError_t launch_sum(const LaunchCtx& c, const double* v, uint64_t n, double* out);
 // stages.cu (batched stage functions of the codec, one thread per block)
 enum StageId { STAGE_NORMALIZE = 1, STAGE_DENORMALIZE, STAGE_MEAN_SLOPE, STAGE_PREDICT, STAGE_QUANTIZE, STAGE_DCT2,
