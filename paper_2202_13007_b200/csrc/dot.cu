@@ -127,13 +127,10 @@ __global__ void __launch_bounds__(128) k_dot_warp(const Basis B, CMat a, CMat b,
 // operation sequence as the single-threaded restatement.  Row stride 9 and
 // slot stride 74 doubles keep the chain reads bank-conflict-free.
 constexpr int RD_WARPS = 2;
-#ifndef RD_MINB
-#define RD_MINB 1
-#endif
 constexpr int RD_SLOT = 74;
 
 template <bool SYM>
-__global__ void __launch_bounds__(RD_WARPS * 32, RD_MINB) k_rowdot(const Basis B, CMat a, CMat b, double* __restrict__ r) {
+__global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a, CMat b, double* __restrict__ r) {
   __shared__ double P[RD_WARPS][32 * RD_SLOT];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* S = P[warp];
@@ -204,8 +201,12 @@ __global__ void __launch_bounds__(RD_WARPS * 32, RD_MINB) k_rowdot(const Basis B
 #define RD_SPLIT 16  // 65536^2: 21.2 ms unsplit, 16.7 / 16.4 / 16.5 ms with 8 / 16 / 32 ranges
 #endif
 
+#ifndef RD_SPLIT_MINB
+#define RD_SPLIT_MINB 1  // (64, 1): 255 registers, 16.8-17.0 ms; plain (64): 220-248 registers, 17.5-17.7 ms
+#endif
+#define RD_SPLIT_BOUNDS __launch_bounds__(RD_WARPS * 32, RD_SPLIT_MINB)
 template <bool SYM>
-__global__ void __launch_bounds__(RD_WARPS * 32, RD_MINB)
+__global__ void RD_SPLIT_BOUNDS
     k_rowdot_split(const Basis B, CMat a, CMat b, double* __restrict__ r, unsigned long long* __restrict__ counter,
                    int* __restrict__ flags, double* __restrict__ state, int nsplit) {
   __shared__ double P[RD_WARPS][32 * RD_SLOT];
