@@ -618,20 +618,23 @@ def test_device_calls_capture_into_cuda_graph():
         dev.decompress(cS, oS)
         dev.decompress(cK, oK)
 
+    def outputs():  # the SoA arrays and dense results (not the layout's padding bytes)
+        return [getattr(m, f) for m in (cA, cB, cS, cK) for f in ("first", "slope", "scale", "coeffs")] + [oS, oK]
+
     cap = torch.cuda.Stream()
     with torch.cuda.stream(cap):
         chain()
     torch.cuda.synchronize()
-    want = [x.clone() for x in (cA.buf, cB.buf, cS.buf, cK.buf, oS, oK)]
-    for x in (cA.buf, cB.buf, cS.buf, cK.buf, oS, oK):
+    want = [x.clone() for x in outputs()]
+    for x in outputs():
         x.zero_()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=cap):
         chain()
     g.replay()
     torch.cuda.synchronize()
-    for x, y in zip((cA.buf, cB.buf, cS.buf, cK.buf, oS, oK), want):
-        assert torch.equal(x.view(torch.uint8), y.view(torch.uint8))
+    for x, y in zip(outputs(), want):
+        assert torch.equal(x.contiguous().view(torch.uint8), y.contiguous().view(torch.uint8))
 
 
 # ---- .blzc container (H/io.hpp:93-134) --------------------------
