@@ -1024,6 +1024,7 @@ blz_block* aos_at(void* base, uint64_t b0, uint64_t bc) { return (blz_block*)bas
 // one call never queue behind another call's large ones (calls from several
 // host threads overlap their PCIe directions).
 const void* mapped_alias(const void* host) {
+  if (reinterpret_cast<uintptr_t>(host) & 7) return nullptr;  // records are read / written as 8-byte words
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
     cudaGetLastError();
