@@ -162,6 +162,8 @@ blz_status blz_dot_entries_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* 
 blz_status blz_rowdot_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, double* r);
 /* Ascending serial sum of n doubles (the Frobenius total from row dots). */
 blz_status blz_sum_dev(blz_ctx* ctx, const double* v, uint64_t n, double* out);
+/* blz_rowdot_dev and the ascending total of r (blz_sum_dev) in one pass: bitwise the same. */
+blz_status blz_rowdot_frobenius_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, double* r, double* total);
 /* mat_mul (H/matrix.hpp:223-235) and mat_mul_dense (:239-250).
  * scratch: device buffer of blz_matmul_scratch_bytes(a,b) bytes. */
 uint64_t blz_matmul_scratch_bytes(const blz_cmat* a, const blz_cmat* b);

@@ -87,6 +87,7 @@ SIGNATURES = {
                                    C.POINTER(blz_cmat)]),
     "blz_matmul_dense_panel_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.c_int, _U64, _P, _P,
                                          _U64]),
+    "blz_rowdot_frobenius_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _P]),
     "blz_reconstruct_rows_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_int, _P]),
     "blz_reconstruct_cols_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_int, _P]),
     "blz_block_mul_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P]),

@@ -605,6 +605,20 @@ blz_status blz_rowdot_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, doub
   return cuda_err(c, blz::launch_rowdot(lc(c), c->basis, view(a), view(b), r, scratch), "mat_rowdot");
 }
 
+// Row dots and their ascending total in one pass (the total follows the groups
+// as they finish inside the split kernel; bitwise blz_rowdot_dev + blz_sum_dev).
+blz_status blz_rowdot_frobenius_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, double* r, double* total) {
+  if (!c || !total) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a, "mat_rowdot")) return st;
+  if (blz_status st = check_cmat(c, b, "mat_rowdot")) return st;
+  if (blz_status st = same_dims(c, a->rows, a->cols, b->rows, b->cols, "mat_rowdot")) return st;
+  if (a->block_rows * a->block_cols == 0) return blz_sum_dev(c, r, 0, total);
+  cudaError_t e;
+  void* scratch = slot(c, S_ROWDOT, blz::rowdot_scratch_bytes(view(a)), &e);
+  if (!scratch) return cuda_err(c, e, "scratch allocation");
+  return cuda_err(c, blz::launch_rowdot(lc(c), c->basis, view(a), view(b), r, scratch, total), "mat_rowdot");
+}
+
 blz_status blz_sum_dev(blz_ctx* c, const double* v, uint64_t n, double* out) {
   if (!c) return BLZ_INVALID_ARGUMENT;
   return cuda_err(c, blz::launch_sum(lc(c), v, n, out), "sum");
@@ -1354,9 +1368,11 @@ blz_status blz_mat_rowdot(blz_ctx* c, const blz_block* a, const blz_block* b, ui
   cudaError_t e;
   double* d = (double*)slot(c, S_OUT, (rows + 1) * sizeof(double), &e);
   if (!d) return cuda_err(c, e, "scratch allocation");
-  if (blz_status st = blz_rowdot_dev(c, &ma, &mb, d)) return st;
-  if (frob)
-    if (blz_status st = blz_sum_dev(c, d, rows, d + rows)) return st;
+  if (frob) {
+    if (blz_status st = blz_rowdot_frobenius_dev(c, &ma, &mb, d, d + rows)) return st;
+  } else if (blz_status st = blz_rowdot_dev(c, &ma, &mb, d)) {
+    return st;
+  }
   BLZ_CUDA(c, cudaMemcpyAsync(r, d, rows * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
   if (frob) BLZ_CUDA(c, cudaMemcpyAsync(frob, d + rows, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
   return latch_status(c);

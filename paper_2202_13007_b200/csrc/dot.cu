@@ -16,6 +16,8 @@
 
 namespace blz {
 
+cudaError_t launch_sum(const LaunchCtx& c, const double* v, uint64_t n, double* out);
+
 template <bool SYM>
 __global__ void __launch_bounds__(128) k_dot_entries(const Basis B, CMat a, CMat b,
                                                      const uint64_t* __restrict__ qi,
@@ -205,11 +207,35 @@ __global__ void __launch_bounds__(RD_WARPS * 32) k_rowdot(const Basis B, CMat a,
 #define RD_SPLIT_MINB 1  // (64, 1): 255 registers, 16.8-17.0 ms; plain (64): 220-248 registers, 17.5-17.7 ms
 #endif
 #define RD_SPLIT_BOUNDS __launch_bounds__(RD_WARPS * 32, RD_SPLIT_MINB)
+// Record slot of one lane (the block it decompresses next), filled by cp.async.
+struct RecSlot {
+  double f, s;
+  uint32_t c[7];
+  uint32_t phiw;  // the 4-byte word holding the scale byte
+};
+
+__device__ __forceinline__ void cpa(void* smem, const void* gmem, int bytes_const8) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes_const8 == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+#ifndef RD_PREFETCH
+#define RD_PREFETCH 1
+#endif
+
 template <bool SYM>
 __global__ void RD_SPLIT_BOUNDS
     k_rowdot_split(const Basis B, CMat a, CMat b, double* __restrict__ r, unsigned long long* __restrict__ counter,
                    int* __restrict__ flags, double* __restrict__ state, int nsplit) {
   __shared__ double P[RD_WARPS][32 * RD_SLOT];
+#if RD_PREFETCH
+  // the next chunk's records, prefetched with cp.async while the current chunk is
+  // decompressed (no registers held in flight)
+  __shared__ RecSlot R[RD_WARPS][2][32];
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* S = P[warp];
   const uint64_t groups = (a.br + 3) / 4;
@@ -218,6 +244,7 @@ __global__ void RD_SPLIT_BOUNDS
   const int dl = lane & 15;
   const int dgrp = dl >> 2, dcol = dl & 3;
   const int cgrp = lane >> 3, u_own = lane & 7;
+  const CMat& src = is_b ? b : a;
   for (;;) {
     unsigned long long w = 0;
     if (lane == 0) w = atomicAdd(counter, 1ull);
@@ -229,6 +256,22 @@ __global__ void RD_SPLIT_BOUNDS
     const uint64_t c0 = (a.bc * (uint64_t)q / nsplit) / 4 * 4;
     const uint64_t c1 = q == nsplit - 1 ? a.bc : (a.bc * (uint64_t)(q + 1) / nsplit) / 4 * 4;
     const uint64_t drow = g * 4 + dgrp, crow = g * 4 + cgrp;
+    const uint64_t dr = min(drow, a.br - 1);
+#if RD_PREFETCH
+    auto prefetch = [&](uint64_t t0, int buf) {
+      const uint64_t idx = dr * a.bc + min(t0 + dcol, a.bc - 1);
+      RecSlot& rs = R[warp][buf][lane];
+      cpa(&rs.f, src.first + idx, 8);
+      cpa(&rs.s, src.slope + idx, 8);
+      const uint32_t* cw = reinterpret_cast<const uint32_t*>(src.coeffs + idx * KEPT);
+#pragma unroll
+      for (int w2 = 0; w2 < 7; ++w2) cpa(&rs.c[w2], cw + w2, 4);
+      cpa(&rs.phiw, reinterpret_cast<const uint32_t*>(src.scale + (idx & ~3ull)), 4);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (c0 < c1) prefetch(c0, 0);
+    int buf = 0;
+#endif
     double acc = 0.0;
     if (q > 0) {  // wait for item (q-1, g), then continue its chains
       if (lane == 0) {
@@ -240,15 +283,35 @@ __global__ void RD_SPLIT_BOUNDS
     }
     for (uint64_t t0 = c0; t0 < c1; t0 += 4) {
       {
-        const uint64_t t = min(t0 + dcol, a.bc - 1), dr = min(drow, a.br - 1);
-        const uint64_t idx = dr * a.bc + t;
         RBlock blk;
-        blk.f = is_b ? b.first[idx] : a.first[idx];
-        blk.s = is_b ? b.slope[idx] : a.slope[idx];
-        blk.phi = is_b ? b.scale[idx] : a.scale[idx];
-        const uint32_t* cw = reinterpret_cast<const uint32_t*>((is_b ? b.coeffs : a.coeffs) + idx * KEPT);
+#if RD_PREFETCH
+        if (t0 + 4 < c1) {
+          prefetch(t0 + 4, buf ^ 1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        {
+          const RecSlot& rs = R[warp][buf][lane];
+          const uint64_t idx = dr * a.bc + min(t0 + dcol, a.bc - 1);
+          blk.f = rs.f;
+          blk.s = rs.s;
+          blk.phi = (rs.phiw >> (8 * (idx & 3))) & 0xffu;
+#pragma unroll
+          for (int w2 = 0; w2 < 7; ++w2) blk.c[w2] = rs.c[w2];
+        }
+        buf ^= 1;
+#else
+        const uint64_t t = min(t0 + dcol, a.bc - 1);
+        const uint64_t idx = dr * a.bc + t;
+        blk.f = src.first[idx];
+        blk.s = src.slope[idx];
+        blk.phi = src.scale[idx];
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(src.coeffs + idx * KEPT);
 #pragma unroll
         for (int w2 = 0; w2 < 7; ++w2) blk.c[w2] = cw[w2];
+#endif
         double* slot = S + lane * RD_SLOT;
         decompress_exact<SYM>(blk, B, [&](int u, const double (&row)[BD]) {
 #pragma unroll
@@ -291,40 +354,53 @@ uint64_t rowdot_scratch_bytes(const CMat& a) {
 }
 
 // Ascending serial sum from +0.0 (the restated oracle's order; inherently one
-// dependent DADD chain).  One thread: the next 32 values are loaded (16-byte
-// loads when aligned) while the current 32 are added, so the chain runs at the
-// DADD latency rather than the load latency.
+// dependent DADD chain).  One warp: the lanes stage batches of 1,024 values in
+// shared memory with cp.async (two buffers, the next batch in flight while the
+// current one is added), lane 0 runs the chain out of shared memory, so the sum
+// proceeds at the DADD latency.
+constexpr int SUM_BATCH = 1024;
+
 __global__ void __launch_bounds__(32) k_sum(const double* __restrict__ v, uint64_t n, double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
-  double s = 0.0;
-  constexpr int G = 32;
-  const uint64_t full = (reinterpret_cast<uintptr_t>(v) & 15) == 0 ? n / G : 0;
-  double cur[G], nxt[G];
-  if (full) {
+  __shared__ __align__(16) double buf[2][SUM_BATCH];
+  const int lane = threadIdx.x & 31;
+  const bool vec = (reinterpret_cast<uintptr_t>(v) & 15) == 0;
+  const uint64_t nfull = vec ? n / SUM_BATCH : 0;  // whole batches
+  auto stage = [&](uint64_t bidx, int slot) {
+    const double* src = v + bidx * SUM_BATCH;
 #pragma unroll
-    for (int k = 0; k < G / 2; ++k) {
-      const double2 p = reinterpret_cast<const double2*>(v)[k];
-      cur[2 * k] = p.x;
-      cur[2 * k + 1] = p.y;
+    for (int k = 0; k < SUM_BATCH / 64; ++k) {  // 16 x 16 bytes per lane
+      const int e = 2 * (k * 32 + lane);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[slot][e]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + e) : "memory");
     }
-  }
-  for (uint64_t g = 0; g < full; ++g) {
-    if (g + 1 < full) {
-      const double2* src = reinterpret_cast<const double2*>(v + (g + 1) * G);
-#pragma unroll
-      for (int k = 0; k < G / 2; ++k) {
-        const double2 p = src[k];
-        nxt[2 * k] = p.x;
-        nxt[2 * k + 1] = p.y;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double s = 0.0;
+  if (nfull) stage(0, 0);
+  for (uint64_t bidx = 0; bidx < nfull; ++bidx) {
+    const int slot = (int)(bidx & 1);
+    if (bidx + 1 < nfull) {
+      stage(bidx + 1, slot ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const double2* p = reinterpret_cast<const double2*>(buf[slot]);
+#pragma unroll 16
+      for (int k = 0; k < SUM_BATCH / 2; ++k) {
+        const double2 x = p[k];
+        s += x.x;
+        s += x.y;
       }
     }
-#pragma unroll
-    for (int k = 0; k < G; ++k) s += cur[k];
-#pragma unroll
-    for (int k = 0; k < G; ++k) cur[k] = nxt[k];
+    __syncwarp();  // the slot is refilled two batches later
   }
-  for (uint64_t k = full * G; k < n; ++k) s += v[k];
-  *out = s;
+  if (lane == 0) {
+    for (uint64_t k = nfull * SUM_BATCH; k < n; ++k) s += v[k];
+    *out = s;
+  }
 }
 
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
@@ -351,7 +427,7 @@ cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a
 }
 
 cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r,
-                          void* scratch) {
+                          void* scratch, double* total) {
   const uint64_t groups = (a.br + 3) / 4;
   const bool sym = c.basis_sym && !c.exact_only;
   // at least 8 chunks of 4 block-columns per range
@@ -374,7 +450,9 @@ cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, con
     else
       k_rowdot_split<false><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r, counter, flags, state, nsplit);
     ++*c.launches;
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (e != cudaSuccess || !total) return e;
+    return launch_sum(c, r, a.rows, total);
   }
   const uint64_t want = (groups + RD_WARPS - 1) / RD_WARPS;
   const uint64_t cap = (uint64_t)c.sm_count * 16;
@@ -384,7 +462,9 @@ cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, con
   else
     k_rowdot<false><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r);
   ++*c.launches;
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !total) return e;
+  return launch_sum(c, r, a.rows, total);
 }
 
 cudaError_t launch_sum(const LaunchCtx& c, const double* v, uint64_t n, double* out) {

@@ -66,8 +66,10 @@ cudaError_t launch_unpack_blzc(const LaunchCtx& c, const uint8_t* in, const CMat
 // dot.cu
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out);
+// total != null: the split kernel also forms the ascending total of r (returns
+// cudaErrorNotSupported when the split kernel does not apply; callers then sum)
 cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r,
-                          void* scratch = nullptr);
+                          void* scratch = nullptr, double* total = nullptr);
 // scratch for the split persistent row-dot kernel (counter, flags, chain state)
 uint64_t rowdot_scratch_bytes(const CMat& a);
 cudaError_t launch_sum(const LaunchCtx& c, const double* v, uint64_t n, double* out);

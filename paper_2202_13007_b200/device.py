@@ -267,8 +267,12 @@ def sum_ascending(v: torch.Tensor, out: torch.Tensor | None = None) -> torch.Ten
 
 
 def frobenius(a: DeviceCMat, b: DeviceCMat):
-    r = rowdot(a, b)
-    return r, sum_ascending(r)
+    """Row dots and their ascending total, in one pass (blz_rowdot_frobenius_dev)."""
+    ctx = context(a.buf.device.index)
+    r = torch.empty(a.rows, dtype=torch.float64, device=a.buf.device)
+    total = torch.empty(1, dtype=torch.float64, device=a.buf.device)
+    ctx.check(ctx.lib.blz_rowdot_frobenius_dev(ctx.handle, a.ref(), b.ref(), _ptr(r), _ptr(total)))
+    return r, total
 
 
 def _tiles(cm: DeviceCMat) -> torch.Tensor:

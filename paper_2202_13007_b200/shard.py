@@ -79,6 +79,8 @@ def rowdot_frobenius(a_local, b_local, group=None):
     """Row dots of the local shard, gathered in row order, and their ascending
     total (bit-exact and deterministic for every world size)."""
     from . import device as dev
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return dev.frobenius(a_local, b_local)  # one pass: the total follows the row dots
     r_local = dev.rowdot(a_local, b_local)
     r_all = gather_uneven(r_local, group)
     return r_all, dev.sum_ascending(r_all)

@@ -518,6 +518,20 @@ def test_rowdot_frobenius_medium(port):
     assert np.float64(tot.item()).view(np.uint64) == np.float64(port.sum_ascending(want)).view(np.uint64)
 
 
+@pytest.mark.parametrize("rows,cols", [(8, 8), (40, 200), (1000, 776), (333, 9000)])
+def test_rowdot_total_one_pass_equals_two_calls(rows, cols):
+    """blz_rowdot_frobenius_dev (row dots with the ascending total formed inside the
+    split kernel, or k_sum after the unsplit one) equals blz_rowdot_dev + blz_sum_dev."""
+    A = dev.compress(W.smooth_field(rows, cols, seed=35, device="cuda"))
+    B = dev.compress(W.rough_uniform(rows, cols, seed=36, device="cuda"))
+    r1, t1 = dev.frobenius(A, B)
+    r2 = dev.rowdot(A, B)
+    t2 = dev.sum_ascending(r2)
+    dev.sync()
+    assert torch.equal(r1.view(torch.int64), r2.view(torch.int64))
+    assert torch.equal(t1.view(torch.int64), t2.view(torch.int64))
+
+
 def test_rowdot_block_row_tail(port):
     """Block-row count not a multiple of 4 and a single block column."""
     for rows, cols in [(40, 8), (13, 3), (72, 70)]:
