@@ -9,11 +9,13 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <filesystem>
 #include <fstream>
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "blaz/blaz.hpp"
@@ -101,46 +103,71 @@ void need(const Args& a, std::size_t npos, bool output) {
     if (!output && !a.output.empty()) throw usage_error(a.cmd + ": takes no --output");
 }
 
-std::ifstream open_input(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw blaz::io_error("cannot open input file: " + path);
-    return in;
+bool has_suffix(const std::string& s, const char* suf) {
+    const std::size_t n = std::strlen(suf);
+    return s.size() >= n && s.compare(s.size() - n, n, suf) == 0;
 }
 
-// temp file + rename: a failed write never leaves a partial output behind
-template <class Write>
-void write_atomically(const std::string& path, bool force, Write&& write) {
-    if (!force && fs::exists(path)) throw blaz::io_error("output exists (use --force to overwrite): " + path);
-    fs::path tmp = path;
-    tmp += ".tmp";
-    {
-        std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
-        if (!out) throw blaz::io_error("cannot open output file: " + tmp.string());
-        write(out);
-        out.flush();
-        if (!out) {
-            std::error_code ec;
-            fs::remove(tmp, ec);
-            throw blaz::io_error("write failed: " + tmp.string());
-        }
-    }
-    std::error_code ec;
-    fs::rename(tmp, path, ec);
-    if (ec) {
-        fs::remove(tmp, ec);
-        throw blaz::io_error("cannot rename temporary file onto " + path);
-    }
+// Parses the file at `path` with `parse(std::istream&)`.
+template <class Parse>
+auto parse_file(const std::string& path, Parse&& parse) {
+    std::ifstream stream(path, std::ios::binary);
+    if (!stream.is_open()) throw blaz::io_error("cannot open input file: " + path);
+    return parse(stream);
 }
 
 blaz::dense_matrix load_dense(const std::string& path) {
-    auto in = open_input(path);
-    if (path.size() >= 4 && path.compare(path.size() - 4, 4, ".csv") == 0) return blaz::import_csv(in);
-    return blaz::read_dense(in);
+    return parse_file(path, [&](std::istream& is) {
+        return has_suffix(path, ".csv") ? blaz::import_csv(is) : blaz::read_dense(is);
+    });
 }
 
 blaz::compressed_matrix load_compressed(const std::string& path) {
-    auto in = open_input(path);
-    return blaz::read_compressed(in);
+    return parse_file(path, [](std::istream& is) { return blaz::read_compressed(is); });
+}
+
+// An output written to "<path>.tmp" and renamed onto <path> by commit(): a
+// failed or abandoned write removes the temporary and never leaves a partial
+// output behind.
+class StagedOutput {
+public:
+    StagedOutput(std::string path, bool force) : final_(std::move(path)), tmp_(final_ + ".tmp") {
+        if (!force && fs::exists(final_))
+            throw blaz::io_error("output exists (use --force to overwrite): " + final_);
+        file_.open(tmp_, std::ios::binary | std::ios::trunc);
+        if (!file_.is_open()) throw blaz::io_error("cannot open output file: " + tmp_.string());
+    }
+    ~StagedOutput() {
+        if (!committed_) {
+            file_.close();
+            std::error_code ignore;
+            fs::remove(tmp_, ignore);
+        }
+    }
+    std::ostream& stream() { return file_; }
+    void commit() {
+        file_.flush();
+        const bool ok = static_cast<bool>(file_);
+        file_.close();
+        if (!ok) throw blaz::io_error("write failed: " + tmp_.string());
+        std::error_code ec;
+        fs::rename(tmp_, final_, ec);
+        if (ec) throw blaz::io_error("cannot rename temporary file onto " + final_);
+        committed_ = true;
+    }
+
+private:
+    std::string final_;
+    fs::path tmp_;
+    std::ofstream file_;
+    bool committed_ = false;
+};
+
+template <class Write>
+void save(const std::string& path, bool force, Write&& write) {
+    StagedOutput out(path, force);
+    write(out.stream());
+    out.commit();
 }
 
 blaz::dense_matrix gen(const std::string& fn, const std::string& ns) {
@@ -205,10 +232,10 @@ long long parse_index(const std::string& s, const char* what) {
 int run(const Args& a) {
     const unsigned th = a.threads;
     auto save_c = [&](const blaz::compressed_matrix& r) {
-        write_atomically(a.output, a.force, [&](std::ostream& o) { blaz::write_compressed(r, o); });
+        save(a.output, a.force, [&](std::ostream& o) { blaz::write_compressed(r, o); });
     };
     auto save_d = [&](const blaz::dense_matrix& r) {
-        write_atomically(a.output, a.force, [&](std::ostream& o) { blaz::write_dense(r, o); });
+        save(a.output, a.force, [&](std::ostream& o) { blaz::write_dense(r, o); });
     };
     if (a.cmd == "gen") {
         need(a, 2, true);
@@ -222,10 +249,16 @@ int run(const Args& a) {
     } else if (a.cmd == "info") {
         need(a, 1, false);
         const blaz::compressed_matrix cm = load_compressed(a.pos[0]);
-        std::printf("dimensions:       %zu x %zu\n", cm.rows, cm.cols);
-        std::printf("block grid:       %zu x %zu (%zu blocks)\n", cm.block_rows, cm.block_cols, cm.blocks.size());
-        std::printf("block payload:    %d bytes\n", blaz::block_payload_bytes);
-        std::printf("compression rate: %.4f\n", blaz::compression_rate);
+        char rate[32];
+        std::snprintf(rate, sizeof rate, "%.4f", blaz::compression_rate);
+        const std::pair<const char*, std::string> fields[] = {
+            {"dimensions", std::to_string(cm.rows) + " x " + std::to_string(cm.cols)},
+            {"block grid", std::to_string(cm.block_rows) + " x " + std::to_string(cm.block_cols) + " (" +
+                               std::to_string(cm.blocks.size()) + " blocks)"},
+            {"block payload", std::to_string(blaz::block_payload_bytes) + " bytes"},
+            {"compression rate", rate},
+        };
+        for (const auto& [name, value] : fields) std::printf("%-18s%s\n", (std::string(name) + ":").c_str(), value.c_str());
     } else if (a.cmd == "add" || a.cmd == "sub") {
         need(a, 2, true);
         const blaz::compressed_matrix x = load_compressed(a.pos[0]), y = load_compressed(a.pos[1]);
@@ -251,7 +284,7 @@ int run(const Args& a) {
         if (a.size.empty() || *end) throw usage_error("--size: not a number: " + a.size);
         if (n < 2) throw argument_error("size must be at least 2");
         const auto rows = blaz::accuracy_suite(n, th);
-        write_atomically(a.output, a.force, [&](std::ostream& o) { blaz::write_accuracy_csv(rows, o); });
+        save(a.output, a.force, [&](std::ostream& o) { blaz::write_accuracy_csv(rows, o); });
     } else if (a.cmd == "bench") {
         need(a, 0, true);
         const auto sizes = parse_sizes(a.sizes);
@@ -261,7 +294,7 @@ int run(const Args& a) {
         if (a.repeats.empty() || *end) throw usage_error("--repeats: not a number: " + a.repeats);
         if (r < 5) throw argument_error("repeats must be at least 5");
         const auto rows = blaz::bench_suite(sizes, ops, int(r), th);
-        write_atomically(a.output, a.force, [&](std::ostream& o) { blaz::write_bench_csv(rows, o); });
+        save(a.output, a.force, [&](std::ostream& o) { blaz::write_bench_csv(rows, o); });
     } else {
         throw usage_error("unknown subcommand '" + a.cmd + "'");
     }
@@ -270,38 +303,28 @@ int run(const Args& a) {
 
 }  // namespace
 
+// Exit status of a failed run: 1 usage, 2 I/O / format / runtime, 3 bad arguments
+// or dimensions (the reference CLI's contract, proj/tools/blaz.cpp).
+int exit_status(const std::exception& e) {
+    if (dynamic_cast<const usage_error*>(&e)) return 1;
+    if (dynamic_cast<const blaz::io_error*>(&e)) return 2;
+    if (dynamic_cast<const argument_error*>(&e) || dynamic_cast<const std::invalid_argument*>(&e) ||
+        dynamic_cast<const std::out_of_range*>(&e))
+        return 3;
+    return 2;
+}
+
 int main(int argc, char** argv) {
     for (int k = 1; k < argc; ++k)
         if (std::string(argv[k]) == "-h" || std::string(argv[k]) == "--help") {
             std::fputs(kUsage, stdout);
             return 0;
         }
-    Args a;
     try {
-        a = parse(argc, argv);
-    } catch (const usage_error& e) {
-        std::fprintf(stderr, "error: %s\n%s", e.what(), kUsage);
-        return 1;
-    }
-    try {
-        return run(a);
-    } catch (const usage_error& e) {
-        std::fprintf(stderr, "error: %s\n%s", e.what(), kUsage);
-        return 1;
-    } catch (const argument_error& e) {
-        std::fprintf(stderr, "error: %s\n", e.what());
-        return 3;
-    } catch (const blaz::io_error& e) {
-        std::fprintf(stderr, "error: %s\n", e.what());
-        return 2;
-    } catch (const std::invalid_argument& e) {
-        std::fprintf(stderr, "error: %s\n", e.what());
-        return 3;
-    } catch (const std::out_of_range& e) {
-        std::fprintf(stderr, "error: %s\n", e.what());
-        return 3;
+        return run(parse(argc, argv));
     } catch (const std::exception& e) {
-        std::fprintf(stderr, "error: %s\n", e.what());
-        return 2;
+        const int status = exit_status(e);
+        std::fprintf(stderr, "error: %s\n%s", e.what(), status == 1 ? kUsage : "");
+        return status;
     }
 }
