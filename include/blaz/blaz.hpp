@@ -31,6 +31,7 @@
 #ifndef BLAZ_DROPIN_BLAZ_HPP
 #define BLAZ_DROPIN_BLAZ_HPP
 
+#include <algorithm>
 #include <array>
 #include <charconv>
 #include <cmath>
@@ -44,6 +45,7 @@
 #include <ostream>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "../blaz_cuda.h"
@@ -498,36 +500,51 @@ inline dense_matrix read_dense(std::istream& in) {
 
 // One matrix row per line, comma-separated decimal cells ('.' separator, blanks
 // around cells allowed); every row must have the same number of cells.
+namespace detail {
+// Cells of one CSV line, each trimmed of spaces / tabs ("a, b" -> {"a", "b"}).
+inline std::vector<std::string_view> csv_cells(std::string_view line) {
+    std::vector<std::string_view> cells;
+    auto trim = [](std::string_view c) {
+        const auto blank = [](char ch) { return ch == ' ' || ch == '\t'; };
+        while (!c.empty() && blank(c.front())) c.remove_prefix(1);
+        while (!c.empty() && blank(c.back())) c.remove_suffix(1);
+        return c;
+    };
+    for (std::size_t start = 0;;) {
+        const std::size_t comma = line.find(',', start);
+        cells.push_back(trim(line.substr(start, comma == std::string_view::npos ? std::string_view::npos : comma - start)));
+        if (comma == std::string_view::npos) return cells;
+        start = comma + 1;
+    }
+}
+}  // namespace detail
+
+// H/io.hpp:155-195: one matrix row per line, comma-separated decimals ('.'), a
+// trailing empty line and CR line ends tolerated; the reference's messages.
 inline dense_matrix import_csv(std::istream& in) {
     std::vector<double> values;
     std::size_t rows = 0, cols = 0;
-    std::string line;
-    while (std::getline(in, line)) {
+    for (std::string line; std::getline(in, line);) {
         if (!line.empty() && line.back() == '\r') line.pop_back();
         if (line.empty() && in.peek() == std::char_traits<char>::eof()) break;
         ++rows;
-        std::size_t cells = 0, pos = 0;
-        for (;;) {
-            const std::size_t comma = line.find(',', pos);
-            const char* b = line.data() + pos;
-            const char* e = line.data() + (comma == std::string::npos ? line.size() : comma);
-            while (b != e && (*b == ' ' || *b == '\t')) ++b;
-            while (e != b && (e[-1] == ' ' || e[-1] == '\t')) --e;
+        const std::vector<std::string_view> cells = detail::csv_cells(line);
+        for (std::size_t c = 0; c < cells.size(); ++c) {
             double v = 0.0;
-            const auto [ptr, ec] = std::from_chars(b, e, v);
-            if (ec != std::errc{} || ptr != e || b == e)
+            const char* first = cells[c].data();
+            const char* last = first + cells[c].size();
+            const auto [ptr, ec] = std::from_chars(first, last, v);
+            if (cells[c].empty() || ec != std::errc{} || ptr != last)
                 throw io_error("csv: non-numeric cell at row " + std::to_string(rows) + ", column " +
-                               std::to_string(cells + 1));
+                               std::to_string(c + 1));
             values.push_back(v);
-            ++cells;
-            if (comma == std::string::npos) break;
-            pos = comma + 1;
         }
-        if (rows == 1)
-            cols = cells;
-        else if (cells != cols)
-            throw io_error("csv: row " + std::to_string(rows) + " has " + std::to_string(cells) + " cells, expected " +
-                           std::to_string(cols));
+        if (rows == 1) {
+            cols = cells.size();
+        } else if (cells.size() != cols) {
+            throw io_error("csv: row " + std::to_string(rows) + " has " + std::to_string(cells.size()) +
+                           " cells, expected " + std::to_string(cols));
+        }
     }
     if (rows == 0) throw io_error("csv: empty input");
     dense_matrix m(rows, cols);
@@ -537,47 +554,57 @@ inline dense_matrix import_csv(std::istream& in) {
 
 // ---- uncompressed baselines (H/matrix.hpp:253-300), CPU ---------------------------
 namespace ref {
+// Dense CPU baselines (H/matrix.hpp:253-300), used by the reference's tests as
+// oracles: each entry is formed by the reference's operation sequence (one
+// rounding per operation, products summed over ascending k from +0.0).
 
 inline void require_same_dims(const dense_matrix& a, const dense_matrix& b, const char* what) {
-    if (a.rows != b.rows || a.cols != b.cols) throw std::invalid_argument(std::string(what) + ": dimension mismatch");
+    if (a.rows == b.rows && a.cols == b.cols) return;
+    throw std::invalid_argument(std::string(what) + ": dimension mismatch");
 }
 
-inline dense_matrix add(const dense_matrix& a, const dense_matrix& b) {
-    require_same_dims(a, b, "ref::add");
+namespace detail {
+template <class Op>
+dense_matrix zip(const dense_matrix& a, const dense_matrix& b, const char* what, Op op) {
+    require_same_dims(a, b, what);
     dense_matrix out(a.rows, a.cols);
-    for (std::size_t k = 0; k < out.values.size(); ++k) out.values[k] = a.values[k] + b.values[k];
+    std::transform(a.values.begin(), a.values.end(), b.values.begin(), out.values.begin(), op);
     return out;
+}
+// sum over k of a_row[k] * b[k * stride], ascending from +0.0
+inline double row_times_column(const double* a_row, const double* b_col, std::size_t n, std::size_t stride) {
+    double acc = 0.0;
+    for (std::size_t k = 0; k < n; ++k, b_col += stride) acc += a_row[k] * *b_col;
+    return acc;
+}
+}  // namespace detail
+
+inline dense_matrix add(const dense_matrix& a, const dense_matrix& b) {
+    return detail::zip(a, b, "ref::add", [](double x, double y) { return x + y; });
 }
 
 inline dense_matrix sub(const dense_matrix& a, const dense_matrix& b) {
-    require_same_dims(a, b, "ref::sub");
-    dense_matrix out(a.rows, a.cols);
-    for (std::size_t k = 0; k < out.values.size(); ++k) out.values[k] = a.values[k] - b.values[k];
-    return out;
+    return detail::zip(a, b, "ref::sub", [](double x, double y) { return x - y; });
 }
 
 inline dense_matrix scale(const dense_matrix& a, double c) {
     dense_matrix out(a.rows, a.cols);
-    for (std::size_t k = 0; k < out.values.size(); ++k) out.values[k] = a.values[k] * c;
+    std::transform(a.values.begin(), a.values.end(), out.values.begin(), [c](double x) { return x * c; });
     return out;
 }
 
 inline double dot(const dense_matrix& a, const dense_matrix& b, std::size_t i, std::size_t j) {
     if (a.cols != b.rows) throw std::invalid_argument("ref::dot: inner dimension mismatch");
     if (i >= a.rows || j >= b.cols) throw std::out_of_range("ref::dot: index out of range");
-    double r = 0.0;
-    for (std::size_t k = 0; k < a.cols; ++k) r += a(i, k) * b(k, j);
-    return r;
+    return detail::row_times_column(a.values.data() + i * a.cols, b.values.data() + j, a.cols, b.cols);
 }
 
 inline dense_matrix mul(const dense_matrix& a, const dense_matrix& b) {
     if (a.cols != b.rows) throw std::invalid_argument("ref::mul: inner dimension mismatch");
     dense_matrix out(a.rows, b.cols);
     for (std::size_t i = 0; i < a.rows; ++i)
-        for (std::size_t k = 0; k < a.cols; ++k) {
-            const double av = a(i, k);
-            for (std::size_t j = 0; j < b.cols; ++j) out(i, j) += av * b(k, j);
-        }
+        for (std::size_t j = 0; j < b.cols; ++j)
+            out(i, j) = detail::row_times_column(a.values.data() + i * a.cols, b.values.data() + j, a.cols, b.cols);
     return out;
 }
 
