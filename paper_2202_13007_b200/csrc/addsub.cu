@@ -5,14 +5,17 @@
 // loaded with coalesced 16-byte accesses into shared memory, combined per lane
 // with exactly the reference's arithmetic, staged and stored coalesced.
 //
-// Exactness of the integer steps:
+// Exactness (combine.cuh):
 //  * int8 -> double: I2F.F64.S8 on a byte lane (exact);
-//  * round_half_away (H/block.hpp:61-67) for |x| < 2^30: k = RN_even(x) is the
-//    low word of x + 1.5*2^52 and fr = x - k is exact.  Exact ties (|fr| = 1/2)
-//    and larger |x| (only when s1 + s2 nearly cancels) send the block's 28
-//    coefficients through the reference's own sequence (clamp_coeff).
+//  * the weight divisions s1 / s, s2 / s, a / p are correctly rounded quotients
+//    from RN reciprocals plus one Markstein correction when the slopes lie in
+//    [2^-400, 2^400]; otherwise IEEE divisions;
+//  * round_half_away + clamp_coeff (H/block.hpp:61-81) for |v| < 2^30 as
+//    sign(v) * min(trunc(RZ(|v| + 1/2)), 127), signs applied four bytes at a
+//    time.  Larger |v| (s1 + s2 nearly cancelling) or NaN weights send the
+//    block's 28 coefficients through the reference's own sequence (clamp_coeff).
 // The s1 + s2 == 0 dense fallback (:36-44) is handed to k_addsub_fallback via
-// the worklist, as before.
+// the worklist.
 #include "blaz_device.cuh"
 #include "combine.cuh"
 #include "fastpath.cuh"

@@ -925,13 +925,15 @@ cudaError_t xfer_h2d(blz_ctx* c, void* dst, const void* src, size_t n, cudaStrea
     if (e != cudaSuccess) return e;
     g.busy = false;
   }
-  if (g.bytes < g.off + n) {
-    // the first piece of a chunk reserves room for the chunk's pieces (add / sub
-    // upload two equal ones); a piece already in the slot is in flight, so the
-    // slot cannot grow mid-chunk
-    if (g.off) return cudaErrorInvalidValue;
+  // the first piece of a chunk reserves room for all of the chunk's pieces (add /
+  // sub upload two equal ones), also when the slot already holds enough for this
+  // piece alone; a piece already in the slot is in flight, so the slot cannot grow
+  // mid-chunk
+  if (g.off == 0) {
     cudaError_t e = stage_reserve(g, (size_t)c->stage_pieces * n);
     if (e != cudaSuccess) return e;
+  } else if (g.bytes < g.off + n) {
+    return cudaErrorInvalidValue;
   }
   char* slotp = (char*)g.p + g.off;
   CopyPool::get().copy(slotp, src, n);

@@ -12,7 +12,7 @@
 //    deterministic, tolerance parity against the exact product.  Two kernels
 //    compute this chain bitwise identically (tests/test_gpu_parity.py checks):
 //      k_gemm_simt<true> (BLZ_GEMM_FUSED_DFMA): the SIMT kernel with DFMA;
-//      k_gemm_dmma (BLZ_GEMM_FUSED_DMMA): FP64 tensor cores (mma.sync m8n8k4
+//      k_gemm_dmma2 (BLZ_GEMM_FUSED_DMMA): FP64 tensor cores (mma.sync m8n8k4
 //      f64).  On B200 one DMMA equals the ascending-k chain of fused
 //      multiply-adds (tools/microbench/dmma_semantics.cu: 0 mismatches in 1.28M
 //      entries).
@@ -148,134 +148,19 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A,
 }
 
 // ---------------------------------------------------------------------------
-// fused DGEMM on FP64 tensor cores (DMMA m8n8k4), ascending k
-// CTA tile 128x128, BK = 32, 8 warps (each 64 x 32: 8 x 4 MMA tiles)
-// ---------------------------------------------------------------------------
-#ifndef DMMA_BK
-#define DMMA_BK 32
-#endif
-constexpr int DBM = 128, DBN = 128, DBK = DMMA_BK;
-constexpr int DAS = DBK + 4;   // As[m][k] row stride = 4 mod 16 doubles: conflict-free fragment loads
-constexpr int DBS = DBN + 4;   // Bs[k][n] row stride = 4 mod 16 doubles
-
-__global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A, uint64_t lda,
-                                                   const double* __restrict__ Bm, uint64_t ldb,
-                                                   double* __restrict__ Cm, uint64_t ldc, uint64_t M,
-                                                   uint64_t N, uint64_t K, bool acc_c) {
-  extern __shared__ __align__(16) double dsm[];
-  double* As0 = dsm;
-  double* Bs0 = dsm + 2 * DBM * DAS;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps: 64 rows x 32 cols each
-  const uint64_t m0 = (uint64_t)blockIdx.y * DBM, n0 = (uint64_t)blockIdx.x * DBN;
-
-  const bool vecA = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-  const bool vecB = ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(Bm) & 15) == 0);
-  auto load_tile = [&](int buf, uint64_t k0) {
-    double* As = As0 + buf * DBM * DAS;
-    double* Bs = Bs0 + buf * DBK * DBS;
-    // A: 128 x DBK doubles in 16-byte chunks (DBK/2 per row)
-#pragma unroll
-    for (int r = 0; r < DBK / 4; ++r) {
-      const int e = tid + r * 256;
-      const int row = e / (DBK / 2), kc = (e % (DBK / 2)) * 2;
-      const uint64_t gr = m0 + row, gk = k0 + kc;
-      double* dst = As + row * DAS + kc;
-      if (vecA && gr < M && gk + 1 < K) {
-        cp_async16(dst, A + gr * lda + gk);
-      } else {
-        dst[0] = (gr < M && gk < K) ? A[gr * lda + gk] : 0.0;
-        dst[1] = (gr < M && gk + 1 < K) ? A[gr * lda + gk + 1] : 0.0;
-      }
-    }
-    // B: DBK x 128 doubles = DBK * 64 16-byte chunks
-#pragma unroll
-    for (int r = 0; r < DBK / 4; ++r) {
-      const int e = tid + r * 256;
-      const int kr = e >> 6, cc = (e & 63) * 2;
-      const uint64_t gk = k0 + kr, gc = n0 + cc;
-      double* dst = Bs + kr * DBS + cc;
-      if (vecB && gk < K && gc + 1 < N) {
-        cp_async16(dst, Bm + gk * ldb + gc);
-      } else {
-        dst[0] = (gk < K && gc < N) ? Bm[gk * ldb + gc] : 0.0;
-        dst[1] = (gk < K && gc + 1 < N) ? Bm[gk * ldb + gc + 1] : 0.0;
-      }
-    }
-    __pipeline_commit();
-  };
-
-  double acc[8][4][2];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {  // D fragment: row = lane>>2, cols = (lane&3)*2 + {0,1}
-      const uint64_t gr = m0 + wm * 64 + i * 8 + (lane >> 2);
-      const uint64_t gc = n0 + wn * 32 + j * 8 + (lane & 3) * 2;
-      acc[i][j][0] = (acc_c && gr < M && gc < N) ? Cm[gr * ldc + gc] : 0.0;
-      acc[i][j][1] = (acc_c && gr < M && gc + 1 < N) ? Cm[gr * ldc + gc + 1] : 0.0;
-    }
-
-  const uint64_t ntiles = (K + DBK - 1) / DBK;
-  load_tile(0, 0);
-  for (uint64_t kt = 0; kt < ntiles; ++kt) {
-    const int buf = (int)(kt & 1);
-    if (kt + 1 < ntiles) {
-      load_tile(buf ^ 1, (kt + 1) * DBK);
-      __pipeline_wait_prior(1);
-    } else {
-      __pipeline_wait_prior(0);
-    }
-    __syncthreads();
-    const double* As = As0 + buf * DBM * DAS;
-    const double* Bs = Bs0 + buf * DBK * DBS;
-#pragma unroll
-    for (int ks = 0; ks < DBK; ks += 4) {
-      double fa[8], fb[4];
-      // A fragment (8x4, row): row = lane>>2, col = lane&3
-#pragma unroll
-      for (int i = 0; i < 8; ++i) fa[i] = As[(wm * 64 + i * 8 + (lane >> 2)) * DAS + ks + (lane & 3)];
-      // B fragment (4x8, col): row = lane&3, col = lane>>2
-#pragma unroll
-      for (int j = 0; j < 4; ++j) fb[j] = Bs[(ks + (lane & 3)) * DBS + wn * 32 + j * 8 + (lane >> 2)];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
-                       : "d"(fa[i]), "d"(fb[j]));
-    }
-    __syncthreads();
-  }
-  // D fragment: row = lane>>2, cols = (lane&3)*2 + {0,1}
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t gr = m0 + wm * 64 + i * 8 + (lane >> 2);
-      const uint64_t gc = n0 + wn * 32 + j * 8 + (lane & 3) * 2;
-      if (gr < M) {
-        if (gc < N) Cm[gr * ldc + gc] = acc[i][j][0];
-        if (gc + 1 < N) Cm[gr * ldc + gc + 1] = acc[i][j][1];
-      }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // fused DGEMM on FP64 tensor cores, small tiles and a deep pipeline (the shape
 // cuBLAS's DGEMM picks on this GPU): CTA tile 64 x 64, BK = 16, 4 cp.async
 // stages, 4 warps (2 x 2, each 32 x 32 = 4 x 4 MMA tiles), several CTAs per SM.
-// Same ascending-k FMA chain per output as k_gemm_dmma and k_gemm_simt<true>
-// (bitwise equal results).  90 % of the DMMA peak at 8192^3 against 80-82 % for
-// the 128 x 128 two-stage k_gemm_dmma (kept as BLZ_GEMM_FUSED_DMMA with G2_USE=0).
+// Same ascending-k FMA chain per output as k_gemm_simt<true> (bitwise equal
+// results).  90 % of the DMMA peak at 8192^3 against 80-82 % for the round-1
+// kernel (128 x 128 tile, BK = 32, two stages, one CTA per SM).
 // ---------------------------------------------------------------------------
 #ifndef G2_STAGES
 #define G2_STAGES 4
 #endif
 // measured at 8192^3 (TFLOP/s): 64x32x16 / 3 stages 32.2; 64x64x16 / 3 31.5, / 4 33.0, / 5-6 31.4;
 // 64x128x16 / 4 32.1; 128x32x16 / 3 30.5; 128x64x16 / 4 22.0; 64x32x32 / 3 29.5; 64x64x8 / 8 32.3;
-// XOR-swizzled unpadded tiles 32.9; the 128x128 two-stage k_gemm_dmma 29.3; cuBLAS DGEMM 35.5
+// XOR-swizzled unpadded tiles 32.9; the round-1 128x128x32 two-stage kernel 29.3; cuBLAS DGEMM 35.5
 #ifndef G2_TM
 #define G2_TM 64
 #endif
@@ -291,15 +176,11 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
 constexpr int G2M = G2_TM, G2N = G2_TN, G2K = G2_TK;
 constexpr int G2MI = G2M / 16, G2NJ = G2N / 16;  // MMA tiles per warp (2 x 2 warps)
 constexpr int G2A_CHUNKS = G2M * G2K / 2 / 128, G2B_CHUNKS = G2K * G2N / 2 / 128;
-#ifndef G2_SWZ
-#define G2_SWZ 0
-#endif
-// G2_SWZ: unpadded tiles with XOR-swizzled 16-byte chunks (the fragment loads of a
-// quarter-warp hit distinct banks); otherwise rows padded by 4 doubles.
-constexpr int G2AS = G2_SWZ ? G2K : G2K + 4;  // As[m][k] row stride
-constexpr int G2BS = G2_SWZ ? G2N : G2N + 4;  // Bs[k][n] row stride
-__device__ __forceinline__ int g2a(int row, int k) { return row * G2AS + (G2_SWZ ? (k ^ ((row & 3) << 2)) : k); }
-__device__ __forceinline__ int g2b(int k, int col) { return k * G2BS + (G2_SWZ ? (col ^ ((k & 3) << 2)) : col); }
+// rows padded by 4 doubles (4 mod 16): the fragment loads of a quarter-warp hit distinct banks
+constexpr int G2AS = G2K + 4;  // As[m][k] row stride
+constexpr int G2BS = G2N + 4;  // Bs[k][n] row stride
+__device__ __forceinline__ int g2a(int row, int k) { return row * G2AS + k; }
+__device__ __forceinline__ int g2b(int k, int col) { return k * G2BS + col; }
 constexpr int G2_STAGE_DOUBLES = G2M * G2AS + G2K * G2BS;
 
 __global__ void __launch_bounds__(128, G2_MINB) k_gemm_dmma2(const double* __restrict__ A, uint64_t lda,
@@ -400,9 +281,6 @@ __global__ void __launch_bounds__(128, G2_MINB) k_gemm_dmma2(const double* __res
     }
 }
 
-#ifndef G2_USE
-#define G2_USE 1
-#endif
 #ifndef FUSED_KERNEL_DEFAULT
 #define FUSED_KERNEL_DEFAULT 2  // BLZ_GEMM_FUSED_DMMA
 #endif
@@ -412,18 +290,12 @@ cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t 
   if (mode == 1) mode = FUSED_KERNEL_DEFAULT;
   // per call: the smem attribute belongs to the current device (a few microseconds
   // against a GEMM of milliseconds)
-  if (mode == 2 && G2_USE) {
+  if (mode == 2) {
     dim3 grid((unsigned)((N + G2N - 1) / G2N), (unsigned)((M + G2M - 1) / G2M));
     const size_t smem = (size_t)G2_STAGES * G2_STAGE_DOUBLES * sizeof(double);
     cudaError_t ea = cudaFuncSetAttribute(k_gemm_dmma2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return ea;
     k_gemm_dmma2<<<grid, 128, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K, acc_c);
-  } else if (mode == 2) {
-    dim3 grid((unsigned)((N + DBN - 1) / DBN), (unsigned)((M + DBM - 1) / DBM));
-    const size_t smem = (size_t)(2 * DBM * DAS + 2 * DBK * DBS) * sizeof(double);
-    cudaError_t ea = cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (ea != cudaSuccess) return ea;
-    k_gemm_dmma<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K, acc_c);
   } else {
     dim3 grid((unsigned)((N + EBN - 1) / EBN), (unsigned)((M + EBM - 1) / EBM));
     const size_t smem = (size_t)(2 * EBM * EAS + 2 * EBK * EBN) * sizeof(double);

@@ -25,6 +25,19 @@ __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+// predicated 16-byte copy (no branch around it)
+__device__ __forceinline__ void cp16_if(bool pred, void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(sa),
+               "l"(gmem), "r"((int)pred)
+               : "memory");
+}
+__device__ __forceinline__ void st16_if(bool pred, void* gmem, uint4 v) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %5, 0; @p st.global.v4.b32 [%0], {%1, %2, %3, %4}; }" ::"l"(gmem),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"((int)pred)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
@@ -32,15 +45,14 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 // block t0; the partial last group is loaded synchronously.
 __device__ __forceinline__ void load_recs(const CMat& m, uint64_t t0, uint64_t nb, int lane, WarpRecs& r) {
   if (t0 + 32 <= nb) {
-    if (lane < 16)
-      cp16(&r.f[2 * lane], m.first + t0 + 2 * lane);
-    else
-      cp16(&r.s[2 * (lane - 16)], m.slope + t0 + 2 * (lane - 16));
-    if (lane < 2) cp16(&r.phi[16 * lane], m.scale + t0 + 16 * lane);
+    // f and s are adjacent in WarpRecs: lanes 0-15 copy f, 16-31 copy s (selects, no branches)
+    const double* fs = lane < 16 ? m.first + t0 + 2 * lane : m.slope + t0 + 2 * (lane - 16);
+    cp16(&r.f[2 * lane], fs);
+    cp16_if(lane < 2, &r.phi[16 * lane], m.scale + t0 + 16 * lane);  // idle lanes: no access
     const uint8_t* src = reinterpret_cast<const uint8_t*>(m.coeffs + t0 * 28);
     uint8_t* dst = reinterpret_cast<uint8_t*>(r.c);
     cp16(dst + 16 * lane, src + 16 * lane);
-    if (lane < 24) cp16(dst + 16 * (32 + lane), src + 16 * (32 + lane));
+    cp16_if(lane < 24, dst + 16 * (32 + lane), src + 16 * (32 + lane));  // idle lanes: no access
   } else {
     const uint64_t t = t0 + lane;
     if (t < nb) {
@@ -57,16 +69,14 @@ __device__ __forceinline__ void load_recs(const CMat& m, uint64_t t0, uint64_t n
 __device__ __forceinline__ void store_recs(const CMat& m, uint64_t t0, uint64_t nb, int lane, const WarpRecs& r) {
   __syncwarp();
   if (t0 + 32 <= nb) {
-    if (lane < 16) {
-      reinterpret_cast<double2*>(m.first + t0)[lane] = reinterpret_cast<const double2*>(r.f)[lane];
-    } else {
-      reinterpret_cast<double2*>(m.slope + t0)[lane - 16] = reinterpret_cast<const double2*>(r.s)[lane - 16];
-    }
+    double* fs = lane < 16 ? m.first + t0 + 2 * lane : m.slope + t0 + 2 * (lane - 16);
+    *reinterpret_cast<double2*>(fs) = reinterpret_cast<const double2*>(r.f)[lane];
     m.scale[t0 + lane] = r.phi[lane];
     const uint4* src = reinterpret_cast<const uint4*>(r.c);
     uint4* dst = reinterpret_cast<uint4*>(m.coeffs + t0 * 28);
     dst[lane] = src[lane];
-    if (lane < 24) dst[32 + lane] = src[32 + lane];
+    const int l2 = lane < 24 ? 32 + lane : lane;  // in-bounds shared read for the idle lanes
+    st16_if(lane < 24, dst + l2, src[l2]);
   } else {
     const uint64_t t = t0 + lane;
     if (t < nb) {

@@ -292,6 +292,25 @@ def test_host_calls_pinned_zero_copy_equal_pageable(rows, cols):
     assert np.array_equal(bits(out[False][5]), bits(out[True][5]))
 
 
+def test_pageable_staging_slot_reuse_across_ops():
+    """A staging slot sized by a one-piece call (scale: one record upload per chunk)
+    must grow before a two-piece call (add: both operands' records per chunk) puts
+    its first piece in it -- on a fresh context, scale then add then sub."""
+    rows = cols = 2040
+    a = W.quadratic_blocks(rows, cols, seed=63).numpy()
+    b = W.quadratic_blocks(rows, cols, seed=64).numpy()
+    A, B = blz.compress_matrix(a), blz.compress_matrix(b)
+    ctx = blz.Context()
+    try:
+        S = blz.mat_scale(A, 0.5, ctx=ctx)
+        got = [blz.mat_add(A, B, ctx=ctx), blz.mat_sub(A, B, ctx=ctx), S]
+    finally:
+        ctx.close()
+    want = [blz.mat_add(A, B), blz.mat_sub(A, B), blz.mat_scale(A, 0.5)]
+    for x, y in zip(got, want):
+        assert blocks_equal(x.blocks, y.blocks)
+
+
 def test_addsub_every_scale_factor_pair(port):
     """add / sub of records covering every (phi1, phi2) pair in [1, 255]^2 (the
     merged scale factor, H/block_ops.hpp:12-15) equal the oracle."""

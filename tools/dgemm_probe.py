@@ -1,5 +1,5 @@
 """cuBLAS DGEMM (torch.matmul, float64) at 8192^3 and 4096^3 as a reference point
-for the hand-written fused GEMM kernels (k_gemm_dmma / k_gemm_simt).
+for the hand-written fused GEMM kernels (k_gemm_dmma2 / k_gemm_simt).
 
     python tools/dgemm_probe.py
 """

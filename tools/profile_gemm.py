@@ -1,4 +1,4 @@
-"""Runs the compressed matmul in each GEMM mode (ncu captures of k_gemm_simt / k_gemm_dmma),
+"""Runs the compressed matmul in each GEMM mode (ncu captures of k_gemm_simt / k_gemm_dmma2),
 and with --time prints CUDA-event ms and TFLOP/s per mode.
 
     python tools/profile_gemm.py [--n 4096] [--time] [--reps 3]
