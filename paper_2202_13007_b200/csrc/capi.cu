@@ -279,6 +279,21 @@ blz_status upload_blocks(blz_ctx* c, const blz_block* h, uint64_t rows, uint64_t
   return blz_unpack_aos_dev(c, (const blz_block*)aos, m);
 }
 
+// One block-column (block index bj of a matrix with nbc block columns) as a
+// rows x ncols matrix (ncols <= 8): a strided host read of one record per block-row.
+blz_status upload_block_col(blz_ctx* c, const blz_block* h, uint64_t rows, uint64_t nbc, uint64_t bj,
+                            uint64_t ncols, int id, blz_cmat* m) {
+  blz_status st = scratch_cmat(c, id, rows, ncols, m);
+  if (st) return st;
+  const uint64_t nb = m->block_rows;
+  cudaError_t e;
+  void* aos = slot(c, S_AUX, nb * sizeof(blz_block), &e);
+  if (!aos) return cuda_err(c, e, "scratch allocation");
+  BLZ_CUDA(c, cudaMemcpy2DAsync(aos, sizeof(blz_block), h + bj, nbc * sizeof(blz_block), sizeof(blz_block), nb,
+                                cudaMemcpyHostToDevice, c->stream), "H2D blocks");
+  return blz_unpack_aos_dev(c, (const blz_block*)aos, m);
+}
+
 blz_status download_blocks(blz_ctx* c, const blz_cmat* m, blz_block* h) {
   const uint64_t nb = m->block_rows * m->block_cols;
   cudaError_t e;
@@ -1212,13 +1227,19 @@ blz_status blz_mat_dot(blz_ctx* c, const blz_block* a, uint64_t ar, uint64_t ac,
   if (!c || !out) return BLZ_INVALID_ARGUMENT;
   if (ac != br) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_dot: inner dimension mismatch");  // H/matrix.hpp:159
   if (i >= ar || j >= bc) return set_err(c, BLZ_OUT_OF_RANGE, "mat_dot: index out of range");  // :160
+  // entry (i, j) reads only block-row i / 8 of a and block-column j / 8 of b
+  // (H/matrix.hpp:162-172): those are uploaded, as a (<= 8) x ac and a br x (<= 8)
+  // matrix, and the entry is (i % 8, j % 8) of their product.
+  const uint64_t bi = i / 8, bj = j / 8;
   blz_cmat ma, mb;
-  if (blz_status st = upload_blocks(c, a, ar, ac, S_CM0, &ma)) return st;
-  if (blz_status st = upload_blocks(c, b, br, bc, S_CM1, &mb)) return st;
+  if (blz_status st = upload_blocks(c, a + bi * ((ac + 7) / 8), std::min<uint64_t>(8, ar - 8 * bi), ac, S_CM0, &ma))
+    return st;
+  if (blz_status st = upload_block_col(c, b, br, (bc + 7) / 8, bj, std::min<uint64_t>(8, bc - 8 * bj), S_CM1, &mb))
+    return st;
   cudaError_t e;
   uint64_t* q = (uint64_t*)slot(c, S_IN0, 4 * sizeof(uint64_t), &e);
   if (!q) return cuda_err(c, e, "scratch allocation");
-  const uint64_t hq[2] = {i, j};
+  const uint64_t hq[2] = {i % 8, j % 8};
   BLZ_CUDA(c, cudaMemcpyAsync(q, hq, sizeof hq, cudaMemcpyHostToDevice, c->stream), "H2D query");
   double* d = (double*)(q + 2);
   if (blz_status st = blz_dot_entries_dev(c, &ma, &mb, q, q + 1, 1, d)) return st;

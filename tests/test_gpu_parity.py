@@ -292,6 +292,21 @@ def test_host_calls_pinned_zero_copy_equal_pageable(rows, cols):
     assert np.array_equal(bits(out[False][5]), bits(out[True][5]))
 
 
+@pytest.mark.parametrize("ar,ac,bc", [(37, 29, 45), (64, 40, 8), (9, 1000, 17)])
+def test_mat_dot_reads_one_block_row_and_column(ar, ac, bc, port):
+    """mat_dot(i, j) uploads only block-row i / 8 of a and block-column j / 8 of b;
+    entries in ragged last block-rows / columns equal the oracle bitwise."""
+    a = W.rough_uniform(ar, ac, seed=71).numpy()
+    b = W.smooth_field(ac, bc, seed=72).numpy()
+    A, B = blz.compress_matrix(a), blz.compress_matrix(b)
+    rng = np.random.default_rng(73)
+    qs = [(0, 0), (ar - 1, bc - 1), (ar - 1, 0), (0, bc - 1)] + [(int(rng.integers(ar)), int(rng.integers(bc))) for _ in range(12)]
+    for i, j in qs:
+        got = blz.mat_dot(A, B, i, j)
+        want = port.mat_dot(A.blocks, ar, ac, B.blocks, ac, bc, i, j)
+        assert np.float64(got).view(np.uint64) == np.float64(want).view(np.uint64), (i, j)
+
+
 def test_pageable_staging_slot_reuse_across_ops():
     """A staging slot sized by a one-piece call (scale: one record upload per chunk)
     must grow before a two-piece call (add: both operands' records per chunk) puts
