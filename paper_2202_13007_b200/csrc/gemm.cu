@@ -4,7 +4,7 @@
 // acc = 0.0; acc += a(i,k) * b(k,j) over the global inner index k ascending
 // (accumulate_product_tile, :188-202), padding excluded (k < a.cols).
 //
-//  * BLZ_GEMM_EXACT -- k_gemm_exact: CUDA-core DMUL + DADD (this TU is built
+//  * BLZ_GEMM_EXACT -- k_gemm_simt<false>: CUDA-core DMUL + DADD (this TU is built
 //    with -fmad=false) in exactly that order: bitwise equal to the reference.
 //    Tiles beyond K are zero-filled: adding +0.0 to a running sum that starts
 //    at +0.0 (and is therefore never -0.0) is the identity.
@@ -17,7 +17,7 @@
 //      multiply-adds (tools/microbench/dmma_semantics.cu: 0 mismatches in 1.28M
 //      entries).
 //    BLZ_GEMM_FUSED runs FUSED_KERNEL_DEFAULT, the faster of the two on B200
-//    (K7, profiles/r02_gemm_dfma_vs_dmma.md).
+//    (K7, profiles/r02_ncu_summary.md).
 #include <cuda_pipeline_primitives.h>
 
 #include "launch.h"
@@ -25,44 +25,47 @@
 namespace blz {
 
 // ---------------------------------------------------------------------------
-// exact SIMT DGEMM: 128x128 CTA tile, BK = 16, 256 threads, 8x8 per thread;
-// both operands staged with cp.async (double buffer), one barrier per 16 k.
+// exact SIMT DGEMM (and its DFMA twin), ascending k, operands staged with
+// cp.async; a warp reads 2 rows of A per k (broadcast) and 256 contiguous bytes
+// of a B row.
 // ---------------------------------------------------------------------------
-constexpr int EBM = 128, EBN = 128, EBK = 16;
-constexpr int EAS = EBK;  // As[m][k] row stride; a warp reads 2 rows per k (broadcast)
+constexpr int EBK = 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   __pipeline_memcpy_async(smem, gmem, 16);
 }
 
 // FMA = false: acc + a*b as DMUL then DADD (-fmad=false); true: one DFMA.
-// ACC: the accumulators start from C (a K-panel continuing the chain of the
-// previous panels: storing and reloading a double is exact, so the per-entry
-// operation sequence is the single-pass one); otherwise from +0.0.
+// The accumulators start from C when acc_c (a K-panel continuing the chain of
+// the previous panels: storing and reloading a double is exact, so the
+// per-entry operation sequence is the single-pass one); otherwise from +0.0.
+// CTA tile 128 x 64 (128 threads, 8 x 8 outputs each), BK = 16, four cp.async
+// stages, two CTAs per SM.  Measured at 8192^3 (TFLOP/s, exact / DFMA): 128x128
+// two stages (round 1) 15.3 / 23.2; 128x64 three stages 15.8 / 24.0, four 16.2 /
+// 24.8; 64x128 four 15.7 / 24.0; 128x128 three 15.2 / 23.1; 64x64 two / three
+// stages (four CTAs per SM) 13.6 / 14.5 exact.
+constexpr int SBM = 128, SBN = 64, STHREADS = SBM * SBN / 64, SSTAGES = 4;
+constexpr int SSTAGE = SBM * EBK + EBK * SBN;
 template <bool FMA>
-__global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A, uint64_t lda,
-                                                    const double* __restrict__ Bm, uint64_t ldb,
-                                                    double* __restrict__ Cm, uint64_t ldc, uint64_t M,
-                                                    uint64_t N, uint64_t K, bool acc_c) {
+__global__ void __launch_bounds__(STHREADS, 2) k_gemm_simt(const double* __restrict__ A, uint64_t lda,
+                                                             const double* __restrict__ Bm, uint64_t ldb,
+                                                             double* __restrict__ Cm, uint64_t ldc, uint64_t M,
+                                                             uint64_t N, uint64_t K, bool acc_c) {
   extern __shared__ __align__(16) double esm[];
-  double* As0 = esm;                      // [2][EBM * EAS]
-  double* Bs0 = esm + 2 * EBM * EAS;      // [2][EBK * EBN]
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
-  const uint64_t m0 = (uint64_t)blockIdx.y * EBM, n0 = (uint64_t)blockIdx.x * EBN;
+  const int tx = tid % (SBN / 8), ty = tid / (SBN / 8);
+  const uint64_t m0 = (uint64_t)blockIdx.y * SBM, n0 = (uint64_t)blockIdx.x * SBN;
   const bool vecA = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   const bool vecB = ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(Bm) & 15) == 0);
-
-  auto load_tile = [&](int buf, uint64_t k0) {
-    double* As = As0 + buf * EBM * EAS;
-    double* Bs = Bs0 + buf * EBK * EBN;
-    // A: 128 rows x 16 k = 1024 double2 chunks -> 4 per thread
+  auto load_tile = [&](int st, uint64_t k0) {
+    double* As = esm + st * SSTAGE;
+    double* Bs = As + SBM * EBK;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int e = tid + r * 256;
+    for (int r = 0; r < SBM * 8 / STHREADS; ++r) {
+      const int e = tid + r * STHREADS;
       const int row = e >> 3, kc = (e & 7) * 2;
       const uint64_t gr = m0 + row, gk = k0 + kc;
-      double* dst = &As[row * EAS + kc];
+      double* dst = &As[row * EBK + kc];
       if (gr < M && gk + 1 < K && vecA) {
         cp_async16(dst, A + gr * lda + gk);
       } else {
@@ -70,13 +73,12 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A,
         dst[1] = (gr < M && gk + 1 < K) ? A[gr * lda + gk + 1] : 0.0;
       }
     }
-    // B: 16 rows x 128 cols = 1024 double2 chunks -> 4 per thread
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int e = tid + r * 256;
-      const int kr = e >> 6, cc = (e & 63) * 2;
+    for (int r = 0; r < 8 * SBN / STHREADS; ++r) {
+      const int e = tid + r * STHREADS;
+      const int kr = e / (SBN / 2), cc = (e % (SBN / 2)) * 2;
       const uint64_t gk = k0 + kr, gc = n0 + cc;
-      double* dst = &Bs[kr * EBN + cc];
+      double* dst = &Bs[kr * SBN + cc];
       if (gk < K && gc + 1 < N && vecB) {
         cp_async16(dst, Bm + gk * ldb + gc);
       } else {
@@ -84,44 +86,40 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A,
         dst[1] = (gk < K && gc + 1 < N) ? Bm[gk * ldb + gc + 1] : 0.0;
       }
     }
-    __pipeline_commit();
   };
-
   double acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const uint64_t gr = m0 + ty * 8 + i, gc = n0 + (j / 2) * 32 + 2 * tx + (j % 2);
+      const uint64_t gr = m0 + ty * 8 + i, gc = n0 + (j / 2) * (SBN / 4) + 2 * tx + (j % 2);
       acc[i][j] = (acc_c && gr < M && gc < N) ? Cm[gr * ldc + gc] : 0.0;
     }
-
   const uint64_t ntiles = (K + EBK - 1) / EBK;
-  load_tile(0, 0);
+#pragma unroll
+  for (int st = 0; st < SSTAGES - 1; ++st) {
+    if ((uint64_t)st < ntiles) load_tile(st, (uint64_t)st * EBK);
+    __pipeline_commit();
+  }
   for (uint64_t kt = 0; kt < ntiles; ++kt) {
-    const int buf = (int)(kt & 1);
-    if (kt + 1 < ntiles) {
-      load_tile(buf ^ 1, (kt + 1) * EBK);
-      __pipeline_wait_prior(1);
-    } else {
-      __pipeline_wait_prior(0);
-    }
+    __pipeline_wait_prior(SSTAGES - 2);
     __syncthreads();
-    const double* As = As0 + buf * EBM * EAS;
-    const double* Bs = Bs0 + buf * EBK * EBN;
+    const uint64_t nt = kt + SSTAGES - 1;
+    if (nt < ntiles) load_tile((int)(nt % SSTAGES), nt * EBK);
+    __pipeline_commit();
+    const double* As = esm + (int)(kt % SSTAGES) * SSTAGE;
+    const double* Bs = As + SBM * EBK;
 #pragma unroll
     for (int kk = 0; kk < EBK; kk += 2) {
-      // two k steps per smem round: A as (k, k+1) pairs, B rows k and k+1
       double2 av[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const double2*>(&As[(ty * 8 + i) * EAS + kk]);
+      for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const double2*>(&As[(ty * 8 + i) * EBK + kk]);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         double bv[8];
-        // thread columns: (j/2)*32 + 2*tx + (j%2) -- 8 lanes read 128 contiguous bytes
 #pragma unroll
         for (int j = 0; j < 8; j += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(&Bs[(kk + h) * EBN + (j / 2) * 32 + 2 * tx]);
+          const double2 v = *reinterpret_cast<const double2*>(&Bs[(kk + h) * SBN + (j / 2) * (SBN / 4) + 2 * tx]);
           bv[j] = v.x;
           bv[j + 1] = v.y;
         }
@@ -133,7 +131,6 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A,
         }
       }
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -141,7 +138,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const double* __restrict__ A,
     if (gr >= M) continue;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const uint64_t gc = n0 + (j / 2) * 32 + 2 * tx + (j % 2);
+      const uint64_t gc = n0 + (j / 2) * (SBN / 4) + 2 * tx + (j % 2);
       if (gc < N) Cm[gr * ldc + gc] = acc[i][j];
     }
   }
@@ -298,12 +295,12 @@ cudaError_t launch_gemm(const LaunchCtx& c, int mode, const double* A, uint64_t 
     if (ea != cudaSuccess) return ea;
     k_gemm_dmma2<<<grid, 128, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K, acc_c);
   } else {
-    dim3 grid((unsigned)((N + EBN - 1) / EBN), (unsigned)((M + EBM - 1) / EBM));
-    const size_t smem = (size_t)(2 * EBM * EAS + 2 * EBK * EBN) * sizeof(double);
+    dim3 grid((unsigned)((N + SBN - 1) / SBN), (unsigned)((M + SBM - 1) / SBM));
+    const size_t smem = (size_t)SSTAGES * SSTAGE * sizeof(double);
     auto kern = mode == 3 ? k_gemm_simt<true> : k_gemm_simt<false>;
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return ea;
-    kern<<<grid, 256, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K, acc_c);
+    kern<<<grid, STHREADS, smem, c.stream>>>(A, lda, Bm, ldb, Cm, ldc, M, N, K, acc_c);
   }
   ++*c.launches;
   return cudaGetLastError();
