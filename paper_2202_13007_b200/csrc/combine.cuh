@@ -89,10 +89,10 @@ __device__ __forceinline__ CombineOut combine_record(double f1, double s1, uint3
     o.phi = phi;
     // Slopes in [2^-400, 2^400] keep every quotient below clear of underflow /
     // overflow, so one IEEE reciprocal of s serves both divisions by s and the
-    // divisions by the scale factors use the table of RN(1/p); each quotient is
-    // then RN(a / b) (div_rcp, tools/microbench/markstein_check.cu).  Otherwise the
-    // plain IEEE divisions.
-    if (mid_range(s1) && mid_range(s2) && mid_range(o.s)) {
+    // divisions by the (nonzero) scale factors use the table of RN(1/p); each
+    // quotient is then RN(a / b) (div_rcp, tools/microbench/markstein_check.cu).
+    // Otherwise (phi = 0 included) the plain IEEE divisions.
+    if (mid_range(s1) && mid_range(s2) && mid_range(o.s) && p1 != 0u && p2 != 0u) {
       const double ys = 1.0 / o.s;
       const double a1 = div_rcp(s1, o.s, ys);        // (:51)
       const double a2 = div_rcp(rhs * s2, o.s, ys);  // (:52)

@@ -405,6 +405,27 @@ def test_records_with_extreme_values(port):
     assert np.array_equal(bits(got), bits(want))
 
 
+def test_addsub_zero_scale_factor(port):
+    """phi = 0 never comes out of compress, but records read from elsewhere may
+    hold it: the weight divisions by 0 (inf / NaN weights, the reference's rounding
+    sequence) equal the oracle for add and sub (non-cancelling slopes)."""
+    rng = np.random.default_rng(81)
+    n = 4096
+    ra, rb = np.zeros(n, blz.BLOCK_DTYPE), np.zeros(n, blz.BLOCK_DTYPE)
+    for r in (ra, rb):
+        r["first"] = rng.normal(size=n)
+        r["slope"] = rng.uniform(0.5, 2.0, size=n) * rng.choice([-1.0, 1.0], size=n)
+        r["scale_factor"] = rng.integers(0, 256, size=n).astype(np.uint8)
+        r["coeffs"] = rng.integers(-127, 128, size=(n, 28)).astype(np.int8)
+    ra["scale_factor"][::3] = 0
+    rb["scale_factor"][1::3] = 0
+    rb["slope"] = np.where(np.abs(ra["slope"] + rb["slope"]) < 0.25, rb["slope"] + 1.0, rb["slope"])
+    A = blz.CompressedMatrix(8 * 64, 8 * 64, ra.reshape(64, 64))
+    B = blz.CompressedMatrix(8 * 64, 8 * 64, rb.reshape(64, 64))
+    for got, want in ((blz.mat_add(A, B).blocks, port.mat_add(ra, rb)), (blz.mat_sub(A, B).blocks, port.mat_sub(ra, rb))):
+        assert blocks_equal(got, want), block_diff_report(got, want)
+
+
 def test_gemm_fused_mode_tolerance(port):
     a = W.smooth_field(64, 96, seed=3).numpy()
     b = W.smooth_field(96, 40, seed=4).numpy()
