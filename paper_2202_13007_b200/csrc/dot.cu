@@ -226,10 +226,60 @@ __device__ __forceinline__ void cpa(void* smem, const void* gmem, int bytes_cons
 #define RD_PREFETCH 1
 #endif
 
+constexpr int SUM_BATCH = 1024;
+
+// The ascending total of the row dots (the restated oracle's order: one dependent
+// DADD chain from +0.0) run by warp 0 of CTA 0 while the other warps still
+// produce row dots: batches of 32 groups (1,024 rows) are staged in shared memory
+// with cp.async as soon as their final flags are up, and lane 0 adds the previous
+// batch meanwhile.  Bitwise the separate k_sum.
+__device__ __noinline__ void rowdot_total_warp(const double* __restrict__ r, uint64_t nrows, uint64_t groups,
+                                  const int* __restrict__ flags, int nsplit, double* __restrict__ buf,
+                                  double* __restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nb = (groups + 31) / 32;
+  double s = 0.0;
+  auto chain = [&](uint64_t bidx) {
+    if (lane == 0) {
+      const double* p = buf + (bidx & 1) * SUM_BATCH;
+      const uint64_t lo = bidx * SUM_BATCH, n = min((uint64_t)SUM_BATCH, nrows - lo);
+      for (uint64_t k = 0; k < n; ++k) s += p[k];
+    }
+  };
+  for (uint64_t bidx = 0; bidx < nb; ++bidx) {
+    const uint64_t g = bidx * 32 + lane;
+    if (g < groups)
+      while (*(volatile const int*)(flags + g) < nsplit) __nanosleep(256);
+    __syncwarp();
+    __threadfence();
+    const uint64_t lo = bidx * SUM_BATCH;
+    double* dst = buf + (bidx & 1) * SUM_BATCH;
+#pragma unroll 4
+    for (int k = 0; k < SUM_BATCH / 32; ++k) {
+      const uint64_t i = lo + (uint64_t)k * 32 + lane;
+      if (i < nrows) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + k * 32 + lane);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(r + i) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (bidx > 0) {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncwarp();
+      chain(bidx - 1);
+      __syncwarp();  // slot (bidx - 1) & 1 is refilled by batch bidx + 1
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+  if (nb) chain(nb - 1);
+  if (lane == 0) *total = s;
+}
+
 template <bool SYM>
 __global__ void RD_SPLIT_BOUNDS
     k_rowdot_split(const Basis B, CMat a, CMat b, double* __restrict__ r, unsigned long long* __restrict__ counter,
-                   int* __restrict__ flags, double* __restrict__ state, int nsplit) {
+                   int* __restrict__ flags, double* __restrict__ state, int nsplit, double* __restrict__ total) {
   __shared__ double P[RD_WARPS][32 * RD_SLOT];
 #if RD_PREFETCH
   // the next chunk's records, prefetched with cp.async while the current chunk is
@@ -245,6 +295,10 @@ __global__ void RD_SPLIT_BOUNDS
   const int dgrp = dl >> 2, dcol = dl & 3;
   const int cgrp = lane >> 3, u_own = lane & 7;
   const CMat& src = is_b ? b : a;
+  if (total && blockIdx.x == 0 && warp == 0) {  // the total, overlapped with the row dots
+    rowdot_total_warp(r, a.rows, groups, flags, nsplit, S, total);
+    return;
+  }
   for (;;) {
     unsigned long long w = 0;
     if (lane == 0) w = atomicAdd(counter, 1ull);
@@ -339,6 +393,11 @@ __global__ void RD_SPLIT_BOUNDS
     if (q == nsplit - 1) {
       const uint64_t row = crow * BD + u_own;
       if (crow < a.br && row < a.rows) r[row] = acc;
+      if (total) {  // publish the group's final row dots to the total warp
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicExch(flags + g, nsplit);
+      }
     } else {
       __stcg(state + g * 32 + lane, acc);
       __threadfence();
@@ -358,8 +417,6 @@ uint64_t rowdot_scratch_bytes(const CMat& a) {
 // shared memory with cp.async (two buffers, the next batch in flight while the
 // current one is added), lane 0 runs the chain out of shared memory, so the sum
 // proceeds at the DADD latency.
-constexpr int SUM_BATCH = 1024;
-
 __global__ void __launch_bounds__(32) k_sum(const double* __restrict__ v, uint64_t n, double* __restrict__ out) {
   __shared__ __align__(16) double buf[2][SUM_BATCH];
   const int lane = threadIdx.x & 31;
@@ -445,14 +502,13 @@ cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, con
     const uint64_t want = (groups * nsplit + RD_WARPS - 1) / RD_WARPS;
     const uint64_t cap = (uint64_t)c.sm_count * (per_sm > 0 ? per_sm : 1);
     const unsigned g = (unsigned)(want < cap ? (want ? want : 1) : cap);
+    // with a total, warp 0 of CTA 0 sums the finished row dots during the run
     if (sym)
-      k_rowdot_split<true><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r, counter, flags, state, nsplit);
+      k_rowdot_split<true><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r, counter, flags, state, nsplit, total);
     else
-      k_rowdot_split<false><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r, counter, flags, state, nsplit);
+      k_rowdot_split<false><<<g, RD_WARPS * 32, 0, c.stream>>>(B, a, b, r, counter, flags, state, nsplit, total);
     ++*c.launches;
-    e = cudaGetLastError();
-    if (e != cudaSuccess || !total) return e;
-    return launch_sum(c, r, a.rows, total);
+    return cudaGetLastError();
   }
   const uint64_t want = (groups + RD_WARPS - 1) / RD_WARPS;
   const uint64_t cap = (uint64_t)c.sm_count * 16;
