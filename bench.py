@@ -578,8 +578,9 @@ def run_extras(args, rank, world):
 
         def allreduce_variant():
             res["t2"] = S.frobenius_allreduce(A, B)
-        ms = _time_dist(gather_variant, args.extra_reps, world)
-        ms_ar = _time_dist(allreduce_variant, args.extra_reps, world)
+        # ~15 ms per call: more repetitions than the GEMM configs at negligible cost
+        ms = _time_dist(gather_variant, max(10, args.extra_reps), world, warm=3)
+        ms_ar = _time_dist(allreduce_variant, max(10, args.extra_reps), world, warm=3)
         pairs = ((n2 + 7) // 8) ** 2
         ach = pairs * FP64_OPS_ROWDOT_PAIR_EXECUTED / (ms * 1e-3) / 1e12
         ach_ref = pairs * FP64_OPS_ROWDOT_PAIR / (ms * 1e-3) / 1e12
