@@ -156,6 +156,15 @@ blz_status blz_scale_decompress_dev(blz_ctx* ctx, const blz_cmat* a, double c, c
  * (an out-of-range index latches BLZ_OUT_OF_RANGE). */
 blz_status blz_dot_entries_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b,
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out);
+/* The same entries against a row shard: a_rows holds rows [row0, row0 + a_rows->rows)
+ * (row0 a multiple of 8) of a matrix with rows_total rows; i are global row
+ * indices.  Entries on rows of other shards are +0.0 (all bits zero), so the
+ * results of all shards combine exactly by an integer sum of their 64-bit
+ * patterns (blz_dot_entries_nccl).  Replaces nothing in the reference: the
+ * batched mat_dot of SURVEY.md 8(e), routed to the rank owning row i. */
+blz_status blz_dot_entries_rows_dev(blz_ctx* ctx, const blz_cmat* a_rows, const blz_cmat* b,
+                                    const uint64_t* i, const uint64_t* j, uint64_t n, uint64_t row0,
+                                    uint64_t rows_total, double* out);
 /* Row-wise dot products (config 2; restated):
  * r[i] = sum_j Ahat(i,j)*Bhat(i,j), ascending j from +0.0, for the rows of a
  * and b (same dims).  r has a->rows entries. */
@@ -194,7 +203,12 @@ blz_status blz_matmul_dense_panel_dev(blz_ctx* ctx, const blz_cmat* a, const blz
  *   frobenius_allreduce: per-rank ascending partials summed by one allreduce
  *     (tolerance parity); r_local has a_local->rows entries;
  *   matmul: config 4 -- gathers B into b_full, then C rows = A rows x B
- *     (H/matrix.hpp:223-235); scratch: blz_matmul_scratch_bytes(a_local, b_full). */
+ *     (H/matrix.hpp:223-235); scratch: blz_matmul_scratch_bytes(a_local, b_full);
+ *   dot_entries: batched mat_dot (H/matrix.hpp:157-173) -- gathers B into
+ *     b_full, each rank evaluates the queries on its own rows of A, and one
+ *     allreduce (integer sum of the 64-bit patterns) gives every rank all n
+ *     entries, bit-identical to the one-GPU result; i, j, out are device arrays
+ *     of n entries (i global row indices, the same on every rank). */
 blz_status blz_allgather_cmat_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* local, const blz_cmat* full);
 blz_status blz_rowdot_frobenius_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local,
                                      const blz_cmat* b_local, uint64_t rows_total, double* r_all, double* total);
@@ -202,6 +216,9 @@ blz_status blz_frobenius_allreduce_nccl(blz_ctx* ctx, void* nccl_comm, const blz
                                         const blz_cmat* b_local, double* r_local, double* total);
 blz_status blz_matmul_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local, const blz_cmat* b_local,
                            const blz_cmat* b_full, int mode, void* scratch, const blz_cmat* c_local);
+blz_status blz_dot_entries_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local, const blz_cmat* b_local,
+                                const blz_cmat* b_full, uint64_t rows_total, const uint64_t* i, const uint64_t* j,
+                                uint64_t n, double* out);
 
 /* AoS (48-byte blz_block, device memory) <-> SoA conversions. */
 blz_status blz_pack_aos_dev(blz_ctx* ctx, const blz_cmat* in, blz_block* out);

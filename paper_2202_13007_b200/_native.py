@@ -109,6 +109,9 @@ SIGNATURES = {
     "blz_sub_decompress_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _U64]),
     "blz_scale_decompress_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat), _P, _U64]),
     "blz_dot_entries_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _P, _U64, _P]),
+    "blz_dot_entries_rows_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _P, _U64, _U64, _U64, _P]),
+    "blz_dot_entries_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat), _U64, _P,
+                                   _P, _U64, _P]),
     "blz_rowdot_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P]),
     "blz_sum_dev": (_ST, [_P, _P, _U64, _P]),
     "blz_matmul_scratch_bytes": (_U64, [C.POINTER(blz_cmat), C.POINTER(blz_cmat)]),

@@ -605,7 +605,21 @@ blz_status blz_dot_entries_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b,
   if (blz_status st = check_cmat(c, a, "mat_dot")) return st;
   if (blz_status st = check_cmat(c, b, "mat_dot")) return st;
   if (a->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_dot: inner dimension mismatch");  // :159
-  return cuda_err(c, blz::launch_dot_entries(lc(c), c->basis, view(a), view(b), i, j, n, out), "mat_dot");
+  return cuda_err(c, blz::launch_dot_entries(lc(c), c->basis, view(a), view(b), i, j, n, out, 0, a->rows),
+                  "mat_dot");
+}
+
+blz_status blz_dot_entries_rows_dev(blz_ctx* c, const blz_cmat* a_rows, const blz_cmat* b, const uint64_t* i,
+                                    const uint64_t* j, uint64_t n, uint64_t row0, uint64_t rows_total,
+                                    double* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  if (blz_status st = check_cmat(c, a_rows, "mat_dot")) return st;
+  if (blz_status st = check_cmat(c, b, "mat_dot")) return st;
+  if (a_rows->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_dot: inner dimension mismatch");
+  if (row0 % 8 != 0 || row0 > rows_total || a_rows->rows > rows_total - row0)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "mat_dot: row shard outside the matrix");
+  return cuda_err(c, blz::launch_dot_entries(lc(c), c->basis, view(a_rows), view(b), i, j, n, out, row0, rows_total),
+                  "mat_dot");
 }
 
 blz_status blz_rowdot_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, double* r) {

@@ -18,20 +18,29 @@ namespace blz {
 
 cudaError_t launch_sum(const LaunchCtx& c, const double* v, uint64_t n, double* out);
 
+// a holds rows [row0, row0 + a.rows) of a matrix with rows_total rows (a row
+// shard; row0 = 0 and rows_total = a.rows for a whole matrix).  Queries on rows
+// of other shards get +0.0 (all bits zero), so the shards' results combine
+// exactly by an integer sum of their bit patterns.
 template <bool SYM>
 __global__ void __launch_bounds__(128) k_dot_entries(const Basis B, CMat a, CMat b,
                                                      const uint64_t* __restrict__ qi,
                                                      const uint64_t* __restrict__ qj, uint64_t n,
                                                      double* __restrict__ out,
-                                                     unsigned long long* err) {
+                                                     unsigned long long* err, uint64_t row0, uint64_t rows_total) {
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
        q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = qi[q], j = qj[q];
-    if (i >= a.rows || j >= b.cols) {
+    const uint64_t ig = qi[q], j = qj[q];
+    if (ig >= rows_total || j >= b.cols) {
       latch_error(err, q, DERR_DOT_RANGE);
       out[q] = 0.0;
       continue;
     }
+    if (ig < row0 || ig - row0 >= a.rows) {  // another shard's row
+      out[q] = 0.0;
+      continue;
+    }
+    const uint64_t i = ig - row0;
     const uint64_t bi = i / BD, bj = j / BD;
     const int ri = (int)(i % BD), cj = (int)(j % BD);
     double r = 0.0;
@@ -69,19 +78,25 @@ __global__ void __launch_bounds__(128) k_dot_entries(const Basis B, CMat a, CMat
 template <bool SYM>
 __global__ void __launch_bounds__(128) k_dot_warp(const Basis B, CMat a, CMat b, const uint64_t* __restrict__ qi,
                                                  const uint64_t* __restrict__ qj, uint64_t n,
-                                                 double* __restrict__ out, unsigned long long* err) {
+                                                 double* __restrict__ out, unsigned long long* err, uint64_t row0,
+                                                 uint64_t rows_total) {
   __shared__ double prod[4][32 * 9];  // per warp: 8 products per lane (+1 pad)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* pw = prod[warp];
   for (uint64_t q = blockIdx.x * (uint64_t)4 + warp; q < n; q += (uint64_t)gridDim.x * 4) {
-    const uint64_t i = qi[q], j = qj[q];
-    if (i >= a.rows || j >= b.cols) {  // warp-uniform
+    const uint64_t ig = qi[q], j = qj[q];
+    if (ig >= rows_total || j >= b.cols) {  // warp-uniform
       if (lane == 0) {
         latch_error(err, q, DERR_DOT_RANGE);
         out[q] = 0.0;
       }
       continue;
     }
+    if (ig < row0 || ig - row0 >= a.rows) {  // another shard's row (k_dot_entries)
+      if (lane == 0) out[q] = 0.0;
+      continue;
+    }
+    const uint64_t i = ig - row0;
     const uint64_t bi = i / BD, bj = j / BD;
     const int ri = (int)(i % BD), cj = (int)(j % BD);
     double r = 0.0;
@@ -461,24 +476,25 @@ __global__ void __launch_bounds__(32) k_sum(const double* __restrict__ v, uint64
 }
 
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
-                               const uint64_t* i, const uint64_t* j, uint64_t n, double* out) {
+                               const uint64_t* i, const uint64_t* j, uint64_t n, double* out, uint64_t row0,
+                               uint64_t rows_total) {
   if (n == 0) return cudaSuccess;
   const bool sym = c.basis_sym && !c.exact_only;
   if (n <= (uint64_t)c.sm_count * 64) {  // few queries: a warp per query
     const unsigned gw = (unsigned)((n + 3) / 4);
     if (sym)
-      k_dot_warp<true><<<gw, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
+      k_dot_warp<true><<<gw, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err, row0, rows_total);
     else
-      k_dot_warp<false><<<gw, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
+      k_dot_warp<false><<<gw, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err, row0, rows_total);
     ++*c.launches;
     return cudaGetLastError();
   }
   const unsigned g = (unsigned)((n + 127) / 128 < (uint64_t)c.sm_count * 16 ? (n + 127) / 128
                                                                              : (uint64_t)c.sm_count * 16);
   if (c.basis_sym && !c.exact_only)
-    k_dot_entries<true><<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
+    k_dot_entries<true><<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err, row0, rows_total);
   else
-    k_dot_entries<false><<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err);
+    k_dot_entries<false><<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, out, c.err, row0, rows_total);
   ++*c.launches;
   return cudaGetLastError();
 }

@@ -65,7 +65,8 @@ cudaError_t launch_pack_blzc(const LaunchCtx& c, const CMat& in, uint8_t* out);
 cudaError_t launch_unpack_blzc(const LaunchCtx& c, const uint8_t* in, const CMat& out, uint64_t nlimit);
 // dot.cu
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
-                               const uint64_t* i, const uint64_t* j, uint64_t n, double* out);
+                               const uint64_t* i, const uint64_t* j, uint64_t n, double* out, uint64_t row0,
+                               uint64_t rows_total);
 // total != null: the split kernel also forms the ascending total of r (returns
 // cudaErrorNotSupported when the split kernel does not apply; callers then sum)
 cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r,

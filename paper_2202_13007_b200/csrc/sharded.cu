@@ -17,6 +17,9 @@
 //                               (tolerance variant)
 //   blz_matmul_nccl             config 4: A row-sharded, compressed B gathered,
 //                               local C rows
+//   blz_dot_entries_nccl        batched mat_dot: B gathered, each query evaluated
+//                               by the rank owning its row, combined by an
+//                               integer-sum allreduce of the 64-bit patterns
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -175,6 +178,26 @@ blz_status blz_matmul_nccl(blz_ctx* c, void* comm, const blz_cmat* a_local, cons
                            const blz_cmat* b_full, int mode, void* scratch, const blz_cmat* c_local) {
   if (blz_status st = blz_allgather_cmat_nccl(c, comm, b_local, b_full)) return st;
   return blz_matmul_dev(c, a_local, b_full, mode, scratch, c_local);
+}
+
+// Every rank: out[q] = (A x B)(i[q], j[q]) for all n queries.  Each rank
+// evaluates the queries on its own rows (others get +0.0, all bits zero), so an
+// allreduce of the 64-bit patterns with an integer sum delivers each entry
+// exactly as its owner computed it.
+blz_status blz_dot_entries_nccl(blz_ctx* c, void* comm, const blz_cmat* a_local, const blz_cmat* b_local,
+                                const blz_cmat* b_full, uint64_t rows_total, const uint64_t* i, const uint64_t* j,
+                                uint64_t n, double* out) {
+  if (!c || !a_local || !b_local || !b_full || (n && (!i || !j || !out))) return BLZ_INVALID_ARGUMENT;
+  int rank = 0, world = 1;
+  if (blz_status st = comm_info(c, comm, &rank, &world)) return st;
+  if (blz_status st = blz_allgather_cmat_nccl(c, comm, b_local, b_full)) return st;
+  const uint64_t br = (rows_total + 7) / 8;
+  const uint64_t row0 = 8 * shard_lo(br, rank, world);
+  if (n == 0) return BLZ_OK;
+  if (blz_status st = blz_dot_entries_rows_dev(c, a_local, b_full, i, j, n, row0, rows_total, out)) return st;
+  cudaStream_t s = (cudaStream_t)blz_ctx_get_stream(c);
+  return nccl_status(c, nccl().allreduce(out, out, n, ncclUint64, ncclSum, (ncclComm_t)comm, s),
+                     "allreduce(dot entries)");
 }
 
 }  // extern "C"

@@ -249,6 +249,21 @@ def dot_entries(a: DeviceCMat, b: DeviceCMat, i: torch.Tensor, j: torch.Tensor) 
     return out
 
 
+def dot_entries_rows(a_rows: DeviceCMat, b: DeviceCMat, i: torch.Tensor, j: torch.Tensor, row0: int,
+                     rows_total: int) -> torch.Tensor:
+    """dot_entries against a row shard: a_rows holds rows [row0, row0 + a_rows.rows)
+    of a rows_total-row matrix, i are global rows; entries on other shards' rows are
+    +0.0 (all bits zero), so shards combine by an integer sum of the bit patterns
+    (blz_dot_entries_rows_dev)."""
+    ctx = context(b.buf.device.index)
+    i = i.to(device=b.buf.device, dtype=torch.int64).contiguous()
+    j = j.to(device=b.buf.device, dtype=torch.int64).contiguous()
+    out = torch.empty(i.numel(), dtype=torch.float64, device=b.buf.device)
+    ctx.check(ctx.lib.blz_dot_entries_rows_dev(ctx.handle, a_rows.ref(), b.ref(), _ptr(i), _ptr(j), i.numel(),
+                                               row0, rows_total, _ptr(out)))
+    return out
+
+
 def rowdot(a: DeviceCMat, b: DeviceCMat, out: torch.Tensor | None = None) -> torch.Tensor:
     ctx = context(a.buf.device.index)
     if out is None:

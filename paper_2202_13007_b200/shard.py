@@ -120,3 +120,34 @@ def matmul(a_local, b_local, b_rows: int, b_cols: int, mode: int = 0, group=None
     from . import device as dev
     b_full = allgather_cmat(b_local, b_rows, b_cols, group, out=b_full)
     return dev.matmul(a_local, b_full, mode=mode, out=out, scratch=scratch)
+
+
+def combine_shard_entries(part: torch.Tensor, group=None) -> torch.Tensor:
+    """Entries computed on one shard (+0.0 where another shard owns the query)
+    combined over the ranks: an integer sum of the 64-bit patterns, so every entry
+    arrives exactly as its owner computed it (-0.0 and NaN payloads included)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return part
+    bits = part.view(torch.int64)
+    if bits.is_cuda and dist.get_backend(group) != "nccl":
+        host = bits.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        return host.to(part.device).view(torch.float64)
+    dist.all_reduce(bits, op=dist.ReduceOp.SUM, group=group)
+    return bits.view(torch.float64)
+
+
+def dot_entries(a_local, b_local, rows_total: int, b_rows: int, b_cols: int, qi, qj, group=None, b_full=None):
+    """Batched mat_dot (H/matrix.hpp:157-173) over row shards: the
+    compressed B is all-gathered, each rank evaluates the queries on its own rows
+    of A, and the entries are combined exactly (combine_shard_entries).  qi are
+    global row indices, the same on every rank; every rank returns all entries,
+    bit-identical to the one-GPU dot_entries."""
+    from . import device as dev
+    rank = dist.get_rank(group) if dist.is_available() and dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    b_all = allgather_cmat(b_local, b_rows, b_cols, group, out=b_full) if world > 1 else b_local
+    r0, _ = local_rows(rows_total, rank, world)
+    part = dev.dot_entries_rows(a_local, b_all, qi, qj, r0, rows_total)
+    return combine_shard_entries(part, group)
+

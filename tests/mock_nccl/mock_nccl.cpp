@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdint>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -94,18 +95,26 @@ ncclResult_t run(Comm* c, const Op& op) {
     const void* src = w.posted[op.root].send;
     if (bytes && src != op.recv && cudaMemcpy(op.recv, src, bytes, cudaMemcpyDeviceToDevice) != cudaSuccess)
       res = ncclUnhandledCudaError;
-  } else if (bytes) {  // sum in rank order (float64 only: what the library reduces)
-    if (op.dtype != ncclFloat64 || op.red != ncclSum) {
+  } else if (bytes) {  // sum in rank order (what the library reduces: float64, and 64-bit integers)
+    const bool f64 = op.dtype == ncclFloat64;
+    const bool i64 = op.dtype == ncclUint64 || op.dtype == ncclInt64;
+    if (!(f64 || i64) || op.red != ncclSum) {
       res = ncclInvalidArgument;
     } else {
       std::vector<double> acc(op.count, 0.0), part(op.count);
+      std::vector<uint64_t> iacc(op.count, 0), ipart(op.count);
       for (int r = 0; r < w.n && res == ncclSuccess; ++r) {
-        if (cudaMemcpy(part.data(), w.posted[r].send, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        if (cudaMemcpy(f64 ? (void*)part.data() : (void*)ipart.data(), w.posted[r].send, bytes,
+                       cudaMemcpyDeviceToHost) != cudaSuccess)
           res = ncclUnhandledCudaError;
-        for (size_t i = 0; i < op.count; ++i) acc[i] = r == 0 ? part[i] : acc[i] + part[i];
+        for (size_t i = 0; i < op.count; ++i) {
+          if (f64) acc[i] = r == 0 ? part[i] : acc[i] + part[i];
+          else iacc[i] += ipart[i];  // two's complement: the same bits for signed and unsigned
+        }
       }
       w.barrier();  // every rank has read every send buffer before any recv (maybe == send) changes
-      if (res == ncclSuccess && cudaMemcpy(op.recv, acc.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+      if (res == ncclSuccess && cudaMemcpy(op.recv, f64 ? (const void*)acc.data() : (const void*)iacc.data(), bytes,
+                                           cudaMemcpyHostToDevice) != cudaSuccess)
         res = ncclUnhandledCudaError;
     }
   }

@@ -35,6 +35,11 @@ Ak = dev.compress(W.smooth_field(rows, inner, seed=83, device="cuda"))   # matmu
 Bk = dev.compress(W.quadratic_blocks(inner, cols, seed=84, device="cuda"))
 r_ref, t_ref = dev.frobenius(A, Bm)
 c_ref = dev.matmul(Ak, Bk, mode=blz.GEMM_EXACT)
+# batched mat_dot queries over every shard (first / last rows and columns included)
+_g = torch.Generator().manual_seed(85)
+q_i = [0, rows - 1, rows - 1, 0] + torch.randint(0, rows, (60,), generator=_g).tolist()
+q_j = [0, cols - 1, 0, cols - 1] + torch.randint(0, cols, (60,), generator=_g).tolist()
+d_ref = dev.dot_entries(Ak, Bk, torch.tensor(q_i), torch.tensor(q_j))
 dev.sync()
 
 
@@ -93,6 +98,15 @@ def rank_main(rank):
         ctx.sync()
         want, _, _ = shard_of(c_ref, rank)
         out["matmul"] = all(torch.equal(getattr(c_l, f), getattr(want, f)) for f in FIELDS)
+        # batched mat_dot: B gathered, each rank's rows, integer-sum combine
+        qi = torch.tensor(q_i, dtype=torch.int64, device="cuda")
+        qj = torch.tensor(q_j, dtype=torch.int64, device="cuda")
+        dots = torch.empty(len(q_i), dtype=torch.float64, device="cuda")
+        b_full2 = dev.DeviceCMat(inner, cols)
+        ctx.check(lib.blz_dot_entries_nccl(h, comm, ak_l.ref(), bk_l.ref(), b_full2.ref(), rows, P(qi), P(qj),
+                                           len(q_i), P(dots)))
+        ctx.sync()
+        out["dot_entries"] = bool(torch.equal(dots.view(torch.int64), d_ref.view(torch.int64)))
         out["rows"] = [r0, nr]
         results[rank] = out
     except Exception as e:  # reported, the test fails on it

@@ -307,6 +307,35 @@ def test_mat_dot_reads_one_block_row_and_column(ar, ac, bc, port):
         assert np.float64(got).view(np.uint64) == np.float64(want).view(np.uint64), (i, j)
 
 
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_dot_entries_row_shards_combine(G):
+    """blz_dot_entries_rows_dev on each block-row shard of A, combined by the integer
+    sum of the 64-bit patterns, equals dot_entries on the whole matrix bitwise
+    (the per-rank half of blz_dot_entries_nccl / shard.dot_entries)."""
+    from paper_2202_13007_b200 import shard as S
+    ar, ac, bc = 8 * 21 + 3, 77, 45
+    A = dev.compress(W.rough_uniform(ar, ac, seed=95, device="cuda"))
+    B = dev.compress(W.smooth_field(ac, bc, seed=96, device="cuda"))
+    g = torch.Generator().manual_seed(97)
+    qi = torch.cat([torch.tensor([0, ar - 1]), torch.randint(0, ar, (200,), generator=g)])
+    qj = torch.cat([torch.tensor([bc - 1, 0]), torch.randint(0, bc, (200,), generator=g)])
+    want = dev.dot_entries(A, B, qi, qj)
+    acc = torch.zeros(qi.numel(), dtype=torch.int64, device="cuda")
+    for r in range(G):
+        lo, hi = S.block_row_range(A.block_rows, r, G)
+        r0, nr = 8 * lo, min(ar, 8 * hi) - 8 * lo
+        sh = dev.DeviceCMat(nr, ac)
+        for f in ("first", "slope", "scale", "coeffs"):
+            getattr(sh, f).copy_(getattr(A, f)[lo * A.block_cols:hi * A.block_cols])
+        acc += dev.dot_entries_rows(sh, B, qi, qj, r0, ar).view(torch.int64)
+    dev.sync()
+    assert torch.equal(acc, want.view(torch.int64))
+    # one rank: shard.dot_entries is the plain call
+    assert torch.equal(S.dot_entries(A, B, ar, ac, bc, qi, qj).view(torch.int64), want.view(torch.int64))
+    with pytest.raises(blz.InvalidArgument, match="row shard outside the matrix"):
+        dev.dot_entries_rows(A, B, qi, qj, 8, ar)
+
+
 def test_pageable_staging_slot_reuse_across_ops():
     """A staging slot sized by a one-piece call (scale: one record upload per chunk)
     must grow before a two-piece call (add: both operands' records per chunk) puts

@@ -36,6 +36,7 @@ def test_sharded_nccl_entry_points_multi_rank(G):
     for rank, out in enumerate(res["ranks"]):
         assert out is not None and "error" not in out, (rank, out)
         assert out["allgather"] and out["rowdot"] and out["frobenius"] and out["matmul"], (rank, out)
+        assert out["dot_entries"], (rank, out)
         assert out["allreduce_rel"] <= 1e-13, (rank, out)  # per-rank partials summed in rank order
         assert out["rows"][0] == rows_seen  # contiguous block-row shards in rank order
         rows_seen += out["rows"][1]

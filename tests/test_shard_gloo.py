@@ -92,3 +92,63 @@ def test_block_row_ranges_partition():
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
             sizes = [h - l for l, h in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _dot_worker(rank, world, port, ar, ac, bc, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from oracle import oracle as O
+        from paper_2202_13007_b200 import shard
+        from paper_2202_13007_b200 import workloads as W
+
+        port_ = O.port()
+        a = W.rough_uniform(ar, ac, seed=91).numpy()
+        b = W.smooth_field(ac, bc, seed=92).numpy()
+        ca, cb = port_.compress_matrix(a), port_.compress_matrix(b)
+        rng = np.random.default_rng(93)
+        qi = [0, ar - 1] + rng.integers(0, ar, 30).tolist()
+        qj = [bc - 1, 0] + rng.integers(0, bc, 30).tolist()
+        r0, nr = shard.local_rows(ar, rank, world)
+        # per-rank entries of the own rows (stand-in for dev.dot_entries_rows): +0.0 elsewhere
+        part = np.zeros(len(qi), np.float64)
+        for k, (i, j) in enumerate(zip(qi, qj)):
+            if r0 <= i < r0 + nr:
+                part[k] = port_.mat_dot(ca, ar, ac, cb, ac, bc, i, j)
+        got = shard.combine_shard_entries(torch.from_numpy(part))
+        # signed zeros and NaN payloads survive the combine bit for bit
+        special = np.array([-0.0, np.nan, 1e-310, -np.inf], np.float64)
+        special.view(np.uint64)[1] |= 0x5A5A
+        sp = np.zeros(len(special) * world, np.float64)
+        sp[rank::world] = special
+        sp_got = shard.combine_shard_entries(torch.from_numpy(sp))
+        if rank == 0:
+            want = [port_.mat_dot(ca, ar, ac, cb, ac, bc, i, j) for i, j in zip(qi, qj)]
+            out_q.put({"got": got.numpy(), "want": np.array(want), "sp": sp_got.numpy(),
+                       "sp_want": np.tile(special, 1)})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_dot_entries_combine_exactly(world):
+    """Batched mat_dot over row shards: each rank's own-row entries, combined by the
+    integer sum of the 64-bit patterns, equal the single-device entries bitwise."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dot_worker, args=(r, world, port, 45, 37, 29, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(res["got"].view(np.uint64), res["want"].view(np.uint64))
+    sp = res["sp"].view(np.uint64).reshape(-1, world)
+    want = res["sp_want"].view(np.uint64)
+    for r in range(world):  # rank r owned entries r, r + world, ...
+        assert np.array_equal(sp[:, r], want)
