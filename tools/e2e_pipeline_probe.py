@@ -25,6 +25,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--rows", type=int, default=16384)
+    ap.add_argument("--timeline", action="store_true", help="print per-call start / end times of the pipelined run")
+    ap.add_argument("--late-s", action="store_true", help="signal the sum's decompression after sub, not after add")
     a = ap.parse_args()
     rows = cols = a.rows
     nbr, nbc = rows // 8, cols // 8
@@ -45,18 +47,30 @@ def main():
     lib = cx.lib
     P = lambda v: v.ctypes.data  # noqa: E731
 
+    log = []
+
+    def timed(who, name, k, fn):
+        s0 = time.perf_counter()
+        fn()
+        log.append((who, name, k, s0, time.perf_counter()))
+
     def upload_side(ctx, k):
         """compress A, scale, compress B, add, sub (uploads and small record ops);
         yields after each result the other side consumes"""
         cA, cB, cS, cD, cK = recs[k % 2]
         h = ctx.handle
-        ctx.check(lib.blz_compress_matrix(h, P(npA), rows, cols, P(cA), 0))
-        ctx.check(lib.blz_mat_scale(h, P(cA), rows, cols, 3.5, P(cK), 0))
+        timed("producer", "compress A", k, lambda: ctx.check(lib.blz_compress_matrix(h, P(npA), rows, cols, P(cA), 0)))
+        timed("producer", "scale", k, lambda: ctx.check(lib.blz_mat_scale(h, P(cA), rows, cols, 3.5, P(cK), 0)))
         yield "k"
-        ctx.check(lib.blz_compress_matrix(h, P(npB), rows, cols, P(cB), 0))
-        ctx.check(lib.blz_mat_add(h, P(cA), rows, cols, P(cB), rows, cols, P(cS), 0))
-        yield "s"
-        ctx.check(lib.blz_mat_sub(h, P(cA), rows, cols, P(cB), rows, cols, P(cD), 0))
+        timed("producer", "compress B", k, lambda: ctx.check(lib.blz_compress_matrix(h, P(npB), rows, cols, P(cB), 0)))
+        timed("producer", "add", k,
+              lambda: ctx.check(lib.blz_mat_add(h, P(cA), rows, cols, P(cB), rows, cols, P(cS), 0)))
+        if not a.late_s:
+            yield "s"
+        timed("producer", "sub", k,
+              lambda: ctx.check(lib.blz_mat_sub(h, P(cA), rows, cols, P(cB), rows, cols, P(cD), 0)))
+        if a.late_s:  # the sum's decompression starts once sub is done: sub's small D2H
+            yield "s"  # does not queue behind a 2 GiB download on the copy engine
         yield "d"
 
     def download_side(ctx, k, wait, tags=("k", "s", "d"), out=None):
@@ -64,8 +78,11 @@ def main():
         cA, cB, cS, cD, cK = recs[k % 2]
         src = {"k": cK, "s": cS, "d": cD}
         for tag in tags:
+            w0 = time.perf_counter()
             wait(tag)
-            ctx.check(lib.blz_decompress_matrix(ctx.handle, P(src[tag]), rows, cols, P(dout if out is None else out), 0))
+            log.append(("consumer", "wait " + tag, k, w0, time.perf_counter()))
+            timed("consumer", "decompress " + tag, k, lambda: ctx.check(
+                lib.blz_decompress_matrix(ctx.handle, P(src[tag]), rows, cols, P(dout if out is None else out), 0)))
 
     def run_pipelined(n, two=False):
         ev = {(k, s): threading.Event() for k in range(n) for s in ("k", "s", "d", "done", "done2")}
@@ -123,6 +140,13 @@ def main():
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / a.steps
         print(f"{name}: {dt * 1e3:.1f} ms per step ({nb / dt / 1e6:.1f} M blocks/s) over {a.steps} steps", flush=True)
+    if a.timeline:
+        log.clear()
+        t0 = time.perf_counter()
+        run_pipelined(a.steps)
+        torch.cuda.synchronize()
+        for who, name, k, s0, s1 in sorted(log, key=lambda e: e[3]):
+            print(f"{who:9s} step {k} {name:12s} {1e3 * (s0 - t0):8.1f} -> {1e3 * (s1 - t0):8.1f} ms ({1e3 * (s1 - s0):6.1f})")
     cx.close()
     cy.close()
     cz.close()
