@@ -718,14 +718,15 @@ cudaError_t launch_compress_pair(const LaunchCtx& c, const FastParams& P, const 
   CUtensorMap tmap{};
   int use_tma = 0;
   if (cols % 256 == 0 && (ld & 1) == 0 && (reinterpret_cast<uintptr_t>(dense) & 15) == 0 && rows >= 8) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
+    // the driver's tensor-map encoder, looked up once (thread-safe static initialisation)
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
       cudaDriverEntryPointQueryResult q;
       void* fn = nullptr;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-          q == cudaDriverEntryPointSuccess)
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
     if (encode) {
       const cuuint64_t dims[3] = {16, cols / 16, rows};
       const cuuint64_t strides[2] = {128, ld * 8};
