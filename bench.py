@@ -634,6 +634,29 @@ def run_extras(args, rank, world):
             rec[mname] = {"ms": round(ms, 3), "tflops": round(tf, 2), "frac_fp64_peak": round(tf / fp64_tflops, 3)}
         rec["exact"]["note"] = "DMUL+DADD in the reference's order: at most 50% of the FP64 FMA peak"
         rec["fused"]["note"] = "FP64 FMA chains (tolerance mode, BLZ_GEMM_FUSED)"
+        if world > 1:
+            # the same product with the all-gather fused into B's decompression: every
+            # rank's shard opened as peer memory (CUDA IPC), read by the kernel itself
+            try:
+                views = S.peer_shards(Bl, n, n)
+                C2 = dev.DeviceCMat(nr, n)
+                ms = _time_dist(lambda: S.matmul_peer(A, views, mode=1, out=C2, scratch=scratch), reps, world)
+                tf = flops / (ms * 1e-3) / 1e12
+                S.matmul(A, Bl, n, n, mode=1, b_full=Bf, out=C, scratch=scratch)
+                dev.sync()
+                same = torch.tensor([0.0 if all(torch.equal(getattr(C, f), getattr(C2, f))
+                                                for f in ("first", "slope", "scale", "coeffs")) else 1.0])
+                import torch.distributed as dist
+                same = same.cuda() if dist.get_backend() == "nccl" else same
+                dist.all_reduce(same)
+                rec["fused_peer_gather"] = {"ms": round(ms, 3), "tflops": round(tf, 2),
+                                            "equals_nccl_path": bool(same.item() == 0),
+                                            "note": "B decompressed straight from the ranks' shards over peer "
+                                                    "memory (blz_matmul_gather_dev): no separate all-gather"}
+                dist.barrier()
+                del views, C2
+            except Exception as e:  # peer access unavailable: the NCCL path above stands
+                rec["fused_peer_gather"] = {"unavailable": repr(e)[:200]}
         rec["peak"] = {"tflops": round(fp64_tflops, 2), "kind": peaks["kind"]}
         if not args.no_parity:
             # C holds the exact-mode result of the last timed call

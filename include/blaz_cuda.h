@@ -216,6 +216,19 @@ blz_status blz_frobenius_allreduce_nccl(blz_ctx* ctx, void* nccl_comm, const blz
                                         const blz_cmat* b_local, double* r_local, double* total);
 blz_status blz_matmul_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local, const blz_cmat* b_local,
                            const blz_cmat* b_full, int mode, void* scratch, const blz_cmat* c_local);
+/* Fused all-gather + decompress: a matrix held as
+ * nshards (<= 16) consecutive block-row shards in separate SoA arrays --
+ * typically the ranks' own shards, opened as peer pointers (CUDA IPC) so the
+ * kernel reads them over NVLink -- decompressed into one dense array (rows =
+ * the shards' rows summed; every shard but the last holds whole block-rows).
+ * blz_matmul_gather_dev: mat_mul with B given as such shards, bitwise equal
+ * to blz_matmul_dev on the whole B (scratch: blz_matmul_scratch_bytes(a, b)
+ * for the whole B's dimensions).  No collective library involved: the
+ * transfer is the decompression kernel's own loads. */
+blz_status blz_decompress_gather_dev(blz_ctx* ctx, const blz_cmat* shards, int nshards, double* dense,
+                                     uint64_t ld);
+blz_status blz_matmul_gather_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b_shards, int nshards, int mode,
+                                 void* scratch, const blz_cmat* out);
 blz_status blz_dot_entries_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local, const blz_cmat* b_local,
                                 const blz_cmat* b_full, uint64_t rows_total, const uint64_t* i, const uint64_t* j,
                                 uint64_t n, double* out);

@@ -109,6 +109,8 @@ SIGNATURES = {
     "blz_sub_decompress_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _U64]),
     "blz_scale_decompress_dev": (_ST, [_P, C.POINTER(blz_cmat), C.c_double, C.POINTER(blz_cmat), _P, _U64]),
     "blz_dot_entries_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _P, _U64, _P]),
+    "blz_decompress_gather_dev": (_ST, [_P, _P, _I, _P, _U64]),
+    "blz_matmul_gather_dev": (_ST, [_P, C.POINTER(blz_cmat), _P, _I, _I, _P, C.POINTER(blz_cmat)]),
     "blz_dot_entries_rows_dev": (_ST, [_P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), _P, _P, _U64, _U64, _U64, _P]),
     "blz_dot_entries_nccl": (_ST, [_P, _P, C.POINTER(blz_cmat), C.POINTER(blz_cmat), C.POINTER(blz_cmat), _U64, _P,
                                    _P, _U64, _P]),

@@ -692,6 +692,68 @@ blz_status blz_matmul_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int 
   return cuda_err(c, blz::launch_compress(lc(c), c->basis, dc, ma, nn, nn, view(out)), "mat_mul compress");
 }
 
+// ---- fused all-gather + decompress over block-row shards (peer memory) --------
+// shards[r] holds block-rows [lo_r, lo_r + shards[r].block_rows) of one matrix, in
+// order; all but the last hold whole block-rows (rows a multiple of 8).
+static blz_status shard_set(blz_ctx* c, const blz_cmat* shards, int n, blz::ShardSet* S, uint64_t* rows,
+                            uint64_t* cols, const char* what) {
+  if (!shards || n < 1 || n > blz::ShardSet::kMax)
+    return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": 1 to 16 shards");
+  S->n = n;
+  S->lo[0] = 0;
+  *rows = 0;
+  *cols = shards[0].cols;
+  for (int r = 0; r < n; ++r) {
+    const blz_cmat& m = shards[r];
+    if (m.block_rows) {
+      if (blz_status st = check_cmat(c, &m, what)) return st;
+    }
+    if (m.cols != *cols || (r + 1 < n && m.rows % 8 != 0))
+      return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": shards do not tile the block-rows");
+    S->part[r] = view(&m);
+    S->lo[r + 1] = S->lo[r] + m.block_rows;
+    *rows += m.rows;
+  }
+  if (*rows == 0) return set_err(c, BLZ_INVALID_ARGUMENT, std::string(what) + ": empty matrix");
+  return BLZ_OK;
+}
+
+blz_status blz_decompress_gather_dev(blz_ctx* c, const blz_cmat* shards, int nshards, double* dense, uint64_t ld) {
+  if (!c || !dense) return BLZ_INVALID_ARGUMENT;
+  blz::ShardSet S;
+  uint64_t rows = 0, cols = 0;
+  if (blz_status st = shard_set(c, shards, nshards, &S, &rows, &cols, "decompress_gather")) return st;
+  if (ld < cols) return set_err(c, BLZ_INVALID_ARGUMENT, "decompress_gather: ld < cols");
+  return cuda_err(c, blz::launch_decompress_gather(lc(c), c->basis, S, (cols + 7) / 8, dense, ld, rows, cols),
+                  "decompress_gather");
+}
+
+blz_status blz_matmul_gather_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b_shards, int nshards, int mode,
+                                 void* scratch, const blz_cmat* out) {
+  if (!c) return BLZ_INVALID_ARGUMENT;
+  blz::ShardSet S;
+  uint64_t brows = 0, bcols = 0;
+  if (blz_status st = shard_set(c, b_shards, nshards, &S, &brows, &bcols, "mat_mul")) return st;
+  if (blz_status st = check_cmat(c, a, "mat_mul")) return st;
+  if (blz_status st = check_cmat(c, out, "mat_mul")) return st;
+  if (a->cols != brows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: inner dimension mismatch");  // :207
+  if (out->rows != a->rows || out->cols != bcols)
+    return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: output dimension mismatch");
+  if (mode < BLZ_GEMM_EXACT || mode > BLZ_GEMM_FUSED_DFMA) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: bad mode");
+  if (!scratch) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_mul: null scratch");
+  const uint64_t ma = 8 * a->block_rows, ka = 8 * a->block_cols, kb = 8 * S.lo[S.n], nn = 8 * ((bcols + 7) / 8);
+  double* da = (double*)scratch;
+  double* db = da + ma * ka;
+  double* dc = db + kb * nn;
+  auto L = lc(c);
+  BLZ_CUDA(c, blz::launch_decompress(L, c->basis, view(a), da, ka, ma, ka), "mat_mul decompress A");
+  // B straight from the shards (the ranks' arrays): no gathered compressed copy
+  BLZ_CUDA(c, blz::launch_decompress_gather(L, c->basis, S, nn / 8, db, nn, kb, nn), "mat_mul decompress B");
+  BLZ_CUDA(c, blz::launch_gemm(L, mode, da, ka, db, nn, dc, nn, ma, nn, a->cols), "mat_mul gemm");
+  if (blz_status st = ensure_worklist(c, a->block_rows * (nn / 8))) return st;
+  return cuda_err(c, blz::launch_compress(lc(c), c->basis, dc, ma, nn, nn, view(out)), "mat_mul compress");
+}
+
 blz_status blz_matmul_dense_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b, int mode, void* scratch,
                                 double* out, uint64_t ld) {
   if (!c) return BLZ_INVALID_ARGUMENT;

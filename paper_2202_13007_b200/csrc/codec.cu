@@ -91,6 +91,42 @@ __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, d
   }
 }
 
+// Fused all-gather + decompress: the same per-block work as k_decompress, the
+// record of block (bi, bj) read from the shard owning block-row bi -- a peer
+// GPU's memory over NVLink when the shards are other ranks' arrays.
+template <bool SYM>
+__global__ void __launch_bounds__(128, 4) k_decompress_gather(const Basis B, const ShardSet S, uint64_t bc,
+                                                              double* __restrict__ dense, uint64_t ld,
+                                                              uint64_t crop_rows, uint64_t crop_cols) {
+  const uint64_t nb = S.lo[S.n] * bc;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+  for (uint64_t base = warp0 * 32; base < nb; base += nwarps * 32) {
+    const uint64_t t = base + lane;
+    const bool valid = t < nb;
+    const uint64_t tt = valid ? t : nb - 1;
+    const uint64_t bi = tt / bc, bj = tt % bc;
+    int r = 0;
+    while (r + 1 < S.n && bi >= S.lo[r + 1]) ++r;
+    const RBlock rb = load_block(S.part[r], (bi - S.lo[r]) * bc + bj);
+    const uint64_t r0 = bi * BD, c0 = bj * BD;
+    const bool full = valid && aligned && r0 + BD <= crop_rows && c0 + BD <= crop_cols;
+    decompress_exact<SYM>(rb, B, [&](int u, const double (&row)[BD]) {
+      if (full) {
+        double2* dst = reinterpret_cast<double2*>(dense + (r0 + u) * ld + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_double2(row[2 * q], row[2 * q + 1]);
+      } else if (valid && r0 + u < crop_rows) {
+#pragma unroll
+        for (int j = 0; j < BD; ++j)
+          if (c0 + j < crop_cols) dense[(r0 + u) * ld + c0 + j] = row[j];
+      }
+    });
+  }
+}
+
 // dequantize_prediction (H/codec.hpp:150-158): the 8x8 slope grid of each
 // block (IDCT of the dequantized coefficients), tile-major output.
 __global__ void __launch_bounds__(128) k_dequantize(const Basis B, CMat in, double* __restrict__ tiles) {
@@ -137,6 +173,17 @@ cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* de
 
 cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in, double* tiles) {
   k_dequantize<<<grid_for(in.nb(), 128, c.sm_count), 128, 0, c.stream>>>(B, in, tiles);
+  ++*c.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decompress_gather(const LaunchCtx& c, const Basis& B, const ShardSet& S, uint64_t bc,
+                                     double* dense, uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
+  const unsigned g = grid_for(S.lo[S.n] * bc, 128, c.sm_count, DEC_GRID_PER_SM);
+  if (c.basis_sym && !c.exact_only)
+    k_decompress_gather<true><<<g, 128, 0, c.stream>>>(B, S, bc, dense, ld, crop_rows, crop_cols);
+  else
+    k_decompress_gather<false><<<g, 128, 0, c.stream>>>(B, S, bc, dense, ld, crop_rows, crop_cols);
   ++*c.launches;
   return cudaGetLastError();
 }

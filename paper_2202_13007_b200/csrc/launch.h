@@ -39,6 +39,16 @@ cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* de
 cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in, double* tiles);
 cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols);
+// A matrix held as consecutive block-row shards in separate SoA arrays (other
+// ranks' shards through peer pointers): part[r] holds block-rows [lo[r], lo[r+1]).
+struct ShardSet {
+  static constexpr int kMax = 16;
+  CMat part[kMax];
+  uint64_t lo[kMax + 1];
+  int n;
+};
+cudaError_t launch_decompress_gather(const LaunchCtx& c, const Basis& B, const ShardSet& S, uint64_t bc,
+                                     double* dense, uint64_t ld, uint64_t crop_rows, uint64_t crop_cols);
 // ops.cu
 cudaError_t launch_addsub_fallback(const LaunchCtx& c, const Basis& B, bool sub, const CMat& a, const CMat& b,
                                    const CMat& out);
@@ -67,8 +77,8 @@ cudaError_t launch_unpack_blzc(const LaunchCtx& c, const uint8_t* in, const CMat
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out, uint64_t row0,
                                uint64_t rows_total);
-// total != null: the split kernel also forms the ascending total of r (returns
-// cudaErrorNotSupported when the split kernel does not apply; callers then sum)
+// total != null: also the ascending total of r (inside the split kernel, or by
+// k_sum after the unsplit one)
 cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r,
                           void* scratch = nullptr, double* total = nullptr);
 // scratch for the split persistent row-dot kernel (counter, flags, chain state)

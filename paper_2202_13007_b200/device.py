@@ -136,6 +136,44 @@ def decompress(cm: DeviceCMat, out: torch.Tensor | None = None) -> torch.Tensor:
     return out
 
 
+def _shard_array(shards):
+    arr = (N.blz_cmat * len(shards))()
+    for k, sh in enumerate(shards):
+        arr[k] = sh.c
+    return arr
+
+
+def decompress_gather(shards, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Decompresses a matrix held as consecutive block-row shards (separate
+    DeviceCMats: the ranks' shards, possibly other GPUs' memory opened as peer
+    views) in one kernel -- the fused all-gather + decompress
+    (blz_decompress_gather_dev)."""
+    dev0 = torch.device("cuda", torch.cuda.current_device())
+    ctx = context(dev0.index)
+    rows, cols = sum(sh.rows for sh in shards), shards[0].cols
+    if out is None:
+        out = torch.empty((rows, cols), dtype=torch.float64, device=dev0)
+    arr = _shard_array(shards)
+    ctx.check(ctx.lib.blz_decompress_gather_dev(ctx.handle, arr, len(shards), _ptr(out), out.stride(0)))
+    return out
+
+
+def matmul_gather(a: DeviceCMat, b_shards, mode: int = N.GEMM_EXACT, out: DeviceCMat | None = None,
+                  scratch: torch.Tensor | None = None) -> DeviceCMat:
+    """mat_mul with B given as block-row shards (blz_matmul_gather_dev): B is
+    decompressed straight from the shards, bitwise the same product as matmul."""
+    ctx = context(a.buf.device.index)
+    b_rows, b_cols = sum(sh.rows for sh in b_shards), b_shards[0].cols
+    if scratch is None:
+        dims = N.blz_cmat(rows=b_rows, cols=b_cols, block_rows=_nb(b_rows), block_cols=_nb(b_cols))
+        n = int(N.load().blz_matmul_scratch_bytes(a.ref(), C.byref(dims)))
+        scratch = torch.empty(n, dtype=torch.uint8, device=a.buf.device)
+    out = out or DeviceCMat(a.rows, b_cols, device=a.buf.device)
+    arr = _shard_array(b_shards)
+    ctx.check(ctx.lib.blz_matmul_gather_dev(ctx.handle, a.ref(), arr, len(b_shards), mode, _ptr(scratch), out.ref()))
+    return out
+
+
 def add(a: DeviceCMat, b: DeviceCMat, out: DeviceCMat | None = None) -> DeviceCMat:
     ctx = context(a.buf.device.index)
     out = out or DeviceCMat(a.rows, a.cols, device=a.buf.device)

@@ -151,3 +151,38 @@ def dot_entries(a_local, b_local, rows_total: int, b_rows: int, b_cols: int, qi,
     part = dev.dot_entries_rows(a_local, b_all, qi, qj, r0, rows_total)
     return combine_shard_entries(part, group)
 
+
+def peer_shards(local, rows: int, cols: int, group=None):
+    """Every rank's block-row shard of a compressed matrix as DeviceCMat views --
+    the other ranks' arrays opened through CUDA IPC, so kernels read them as peer
+    memory over NVLink (or plain device memory when ranks share a GPU).  A
+    collective, done once per buffer like communicator setup: the views alias
+    the ranks' live buffers, which must stay allocated while they are used."""
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    from . import device as dev
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    handles = [None] * world
+    dist.all_gather_object(handles, reduce_tensor(local.buf), group=group)
+    views = []
+    for r, (rebuild, args) in enumerate(handles):
+        buf = local.buf if r == rank else rebuild(*args)
+        _, nr = local_rows(rows, r, world)
+        views.append(local if r == rank else dev.DeviceCMat(nr, cols, buf=buf))
+    return views
+
+
+def matmul_peer(a_local, b_views, mode: int = 0, group=None, out=None, scratch=None):
+    """Config 4 without a gather: this rank's C rows = its A rows x B, where B is
+    decompressed straight from all ranks' shards (peer_shards) by one kernel --
+    the all-gather fused into the decompression (blz_matmul_gather_dev), bitwise
+    the result of matmul().  The shards must be complete on every rank first (a
+    device sync and a barrier here), and no rank may overwrite its shard before
+    the others' products are done (the caller's barrier)."""
+    from . import device as dev
+    torch.cuda.synchronize()
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier(group)
+    return dev.matmul_gather(a_local, b_views, mode, out=out, scratch=scratch)
+
