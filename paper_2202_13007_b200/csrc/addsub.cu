@@ -25,9 +25,6 @@
 #ifndef ASB_GRID_PER_SM
 #define ASB_GRID_PER_SM 96  // many short CTAs beat a resident grid (6/SM: 0.142 ms, 96: 0.126 ms)
 #endif
-#ifndef ASB_MINB
-#define ASB_MINB 1
-#endif
 #ifndef SCL_GRID_PER_SM
 #define SCL_GRID_PER_SM 32
 #endif
