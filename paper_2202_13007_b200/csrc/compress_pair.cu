@@ -67,6 +67,7 @@ struct Butterfly {
 #define CP_TMA_ROWS 3
 #endif
 
+
 struct PairShared {
   double sumA[32];
   double amax[2][32];
@@ -210,12 +211,11 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
   }
   __syncthreads();
   uint32_t tphase = 0;
-  auto tma_ok = [&](uint64_t gg, const BlockCursor& cc) -> bool {
-    const uint64_t bi0 = __shfl_sync(0xffffffffu, cc.bi, 0);
+  // group gg starts at lane 0's cursor block (bi0, bj0)
+  auto tma_ok = [&](uint64_t gg, uint64_t bi0) -> bool {
     return use_tma && gg < groups && gg * 32 + 32 <= nb && bi0 * BD + BD <= rows;
   };
-  auto tma_issue = [&](const BlockCursor& cc) {
-    const uint64_t bi0 = __shfl_sync(0xffffffffu, cc.bi, 0), bj0 = __shfl_sync(0xffffffffu, cc.bj, 0);
+  auto tma_issue = [&](uint64_t bi0, uint64_t bj0) {
     if (lane == 0) {
       const unsigned dst = (unsigned)__cvta_generic_to_shared(&stile[warp][0]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -228,8 +228,12 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
           : "memory");
     }
   };
-  bool staged = tma_ok(g0, cur);
-  if (staged) tma_issue(cur);
+  bool staged;
+  {
+    const uint64_t bi0 = __shfl_sync(0xffffffffu, cur.bi, 0), bj0 = __shfl_sync(0xffffffffu, cur.bj, 0);
+    staged = tma_ok(g0, bi0);
+    if (staged) tma_issue(bi0, bj0);
+  }
   const int swz_line = lane >> 1, swz_x = (lane >> 1) & 7, swz_c = (lane & 1) * 4;
 #endif
   for (uint64_t g = g0; g < groups; g += gstep, cur.advance(out.bc)) {
@@ -316,10 +320,11 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
 #if CP_TMA
     BlockCursor tnx = cur;
     tnx.advance(out.bc);
-    const bool staged_next = tma_ok(g + gstep, tnx);
+    const uint64_t nbi0 = __shfl_sync(0xffffffffu, tnx.bi, 0), nbj0 = __shfl_sync(0xffffffffu, tnx.bj, 0);
+    const bool staged_next = tma_ok(g + gstep, nbi0);
     if (staged_next) {  // own buffer: free once every lane has read it
       __syncwarp();
-      tma_issue(tnx);
+      tma_issue(nbi0, nbj0);
     }
 #endif
 
