@@ -125,6 +125,17 @@ def test_ragged_shapes(port, rows, cols):
     assert np.array_equal(bits(back), bits(port.decompress_matrix(oa, rows, cols)))
 
 
+@pytest.mark.parametrize("rows,cols", [(1003, 512), (77, 768), (8, 256), (520, 2304)])
+def test_compress_tma_shapes(port, rows, cols):
+    """Column counts that are multiples of 256 take the TMA tile loads (whole groups
+    of 32 blocks in one block-row); ragged last block-rows and tail groups take the
+    direct loads in the same launch.  Bitwise equal to the oracle."""
+    for a in (W.smooth_field(rows, cols, seed=rows + cols).numpy(), W.quadratic_blocks(rows, cols, seed=cols).numpy()):
+        ca = blz.compress_matrix(a)
+        oa = port.compress_matrix(a)
+        assert blocks_equal(ca.blocks, oa), block_diff_report(ca.blocks, oa)
+
+
 def test_errors_match_reference():
     with pytest.raises(blz.InvalidArgument, match="compress_matrix: empty matrix"):
         blz.compress_matrix(np.zeros((0, 4)))
