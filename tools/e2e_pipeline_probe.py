@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--rows", type=int, default=16384)
     ap.add_argument("--timeline", action="store_true", help="print per-call start / end times of the pipelined run")
     ap.add_argument("--late-s", action="store_true", help="signal the sum's decompression after sub, not after add")
+    ap.add_argument("--pageable", action="store_true", help="plain (pageable) host buffers instead of pinned ones")
     a = ap.parse_args()
     rows = cols = a.rows
     nbr, nbc = rows // 8, cols // 8
@@ -36,13 +37,25 @@ def main():
     hA.copy_(W.make("quadratic", rows, cols, seed=1, device="cuda"))
     hB.copy_(W.make("quadratic", rows, cols, seed=2, device="cuda"))
     npA, npB = hA.numpy(), hB.numpy()
+    if a.pageable:
+        import numpy as np
+        npA, npB = np.array(npA), np.array(npB)
 
     def pinned_blocks():
+        if a.pageable:
+            import numpy as np
+            return np.zeros(nb, blz.BLOCK_DTYPE)
         return torch.empty(nb * 48, dtype=torch.uint8, pin_memory=True).numpy().view(blz.BLOCK_DTYPE)
 
+    def dense_out():
+        if a.pageable:
+            import numpy as np
+            return np.empty((rows, cols), np.float64)
+        return torch.empty((rows, cols), dtype=torch.float64, pin_memory=True).numpy()
+
     recs = [[pinned_blocks() for _ in range(5)] for _ in range(2)]  # cA cB cS cD cK per parity
-    dout = torch.empty((rows, cols), dtype=torch.float64, pin_memory=True).numpy()
-    dout2 = torch.empty((rows, cols), dtype=torch.float64, pin_memory=True).numpy()
+    dout = dense_out()
+    dout2 = dense_out()
     cx, cy, cz = blz.Context(0), blz.Context(0), blz.Context(0)
     lib = cx.lib
     P = lambda v: v.ctypes.data  # noqa: E731
