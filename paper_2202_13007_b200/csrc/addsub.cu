@@ -69,13 +69,10 @@ __global__ void __launch_bounds__(128) k_addsub_v2(CMat a, CMat b, CMat out, uin
     const uint64_t t = t0 + lane;
     const double f1 = ra.f[lane], f2 = rb.f[lane], s1 = ra.s[lane], s2 = rb.s[lane];
     const uint32_t p1 = ra.phi[lane], p2 = rb.phi[lane];
-    uint32_t c1[7], c2[7];
-#pragma unroll
-    for (int w = 0; w < 7; ++w) {
-      c1[w] = ra.c[lane * 7 + w];
-      c2[w] = rb.c[lane * 7 + w];
-    }
-    const CombineOut o = combine_record<SUB>(f1, s1, p1, c1, f2, s2, p2, c2);
+    // the coefficient words straight from the staged records (each branch of the
+    // combine loads what it uses; register copies between the branches cost 5 %)
+    const CombineOut o = combine_record<SUB>(f1, s1, p1, SmemWords{&ra.c[lane * 7]}, f2, s2, p2,
+                                             SmemWords{&rb.c[lane * 7]});
     const bool fallback = o.fallback, slow = o.slow;
     const double of = o.f, os = o.s, w1 = o.w1, w2 = o.w2;
     const uint32_t ophi = o.phi;

@@ -50,9 +50,17 @@ __device__ __forceinline__ bool mid_range(double x) {
   return h > __int_as_float(0x26f00000) && h < __int_as_float(0x58f00000);
 }
 
-template <bool SUB>
-__device__ __forceinline__ CombineOut combine_record(double f1, double s1, uint32_t p1, const uint32_t (&c1)[7],
-                                                     double f2, double s2, uint32_t p2, const uint32_t (&c2)[7]) {
+// The coefficient words come as arrays in registers or as a view of shared
+// memory (SmemWords): each branch then loads the words it uses, instead of the
+// compiler moving register copies between the branches.
+struct SmemWords {
+  const uint32_t* p;
+  __device__ __forceinline__ uint32_t operator[](int w) const { return p[w]; }
+};
+
+template <bool SUB, class W1, class W2>
+__device__ __forceinline__ CombineOut combine_record(double f1, double s1, uint32_t p1, const W1& c1, double f2,
+                                                     double s2, uint32_t p2, const W2& c2) {
   CombineOut o;
   const double rhs = SUB ? -1.0 : 1.0;
   o.f = f1 + rhs * f2;  // (:22)
