@@ -57,6 +57,12 @@ def test_gather_decompress_and_matmul_from_shards(world):
     with pytest.raises(blz.InvalidArgument, match="shards do not tile"):
         bad = dev.DeviceCMat(8 * 3 + 1, n)  # a non-final shard with a partial block-row
         dev.decompress_gather([bad, shards[-1]])
+    with pytest.raises(blz.InvalidArgument, match="shards do not tile"):
+        dev.decompress_gather([shards[0], dev.DeviceCMat(8, n + 8)])  # column counts differ
+    with pytest.raises(blz.InvalidArgument, match="mat_mul: inner dimension mismatch"):
+        dev.matmul_gather(A, shards[:-1] if world > 1 else [dev.DeviceCMat(8, n)])
+    with pytest.raises(blz.InvalidArgument, match="1 to 16 shards"):
+        dev.decompress_gather([shards[0]] * 17)
 
 
 def _free_port():
