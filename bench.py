@@ -1045,7 +1045,7 @@ def main():
     ap.add_argument("--ref-sample-rows", type=int, default=0,
                     help="reference arm: rows of the workload timed (0 = all of it, the default)")
     ap.add_argument("--cpu-sample-rows", type=int, default=2048, help="our arm's bounded cpu_baseline sample")
-    ap.add_argument("--cpu-repeats", type=int, default=3)
+    ap.add_argument("--cpu-repeats", type=int, default=5)
     ap.add_argument("--no-extras", action="store_true", help="skip the config-2/3/4 measurements")
     ap.add_argument("--cfg2-size", type=int, default=65536)
     ap.add_argument("--cfg3-size", type=int, default=8192)
