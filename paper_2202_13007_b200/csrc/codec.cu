@@ -8,7 +8,7 @@
 #include "launch.h"
 
 #ifndef DEC_GRID_PER_SM
-#define DEC_GRID_PER_SM 64
+#define DEC_GRID_PER_SM 128  // short-lived CTAs: 4 / 8 / 32 / 64 / 128 / 256 per SM: 0.589 / 0.586 / 0.575 / 0.561 / 0.560 / 0.568 ms
 #endif
 
 namespace blz {
