@@ -926,6 +926,8 @@ class CopyPool {
   }
   // memcpy(dst, src, n) split over the pool and the calling thread
   void copy(void* dst, const void* src, size_t n) {
+    // 4 MB pieces (1 / 2 MB: faster for 12 MB record chunks, slower for small
+    // calls -- waking the pool costs more than it saves there)
     const size_t piece_min = size_t(4) << 20;
     const int parts = (int)std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, n / piece_min));
     if (parts <= 1) {
@@ -1075,11 +1077,22 @@ cudaError_t drain(blz_ctx::Stage& g) {
   return e;
 }
 
+// Chunks: about 16 per call, each a multiple of 16 block-rows (16-byte aligned SoA
+// sub-views) and moving at least kChunkMinBytes, so that small calls are not
+// dominated by per-chunk synchronisation.
+constexpr uint64_t kChunkMinBytes = uint64_t(8) << 20;
+
 template <class H2D, class Compute, class D2H>
-blz_status pipelined_body(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compute, D2H&& d2h) {
+blz_status pipelined_body(blz_ctx* c, uint64_t block_rows, uint64_t bytes_per_block_row, H2D&& h2d, Compute&& compute,
+                          D2H&& d2h) {
   uint64_t step = (block_rows + 15) / 16;
   step = (step + 15) / 16 * 16;
   if (step < 16) step = 16;
+  if (bytes_per_block_row) {
+    uint64_t min_step = (kChunkMinBytes + bytes_per_block_row - 1) / bytes_per_block_row;
+    min_step = (min_step + 15) / 16 * 16;
+    if (step < min_step) step = min_step;
+  }
   const uint64_t nchunks = (block_rows + step - 1) / step;
   if (blz_status st = ensure_pipe(c, 2 * nchunks + 1)) return st;
   // uploads must not overtake earlier work queued on the context stream
@@ -1118,8 +1131,9 @@ blz_status pipelined_body(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& 
 // Runs the chunk pipeline and always drains all three streams before returning,
 // so no copy touches the caller's host buffers after the call (also on errors).
 template <class H2D, class Compute, class D2H>
-blz_status pipelined(blz_ctx* c, uint64_t block_rows, H2D&& h2d, Compute&& compute, D2H&& d2h) {
-  const blz_status st = pipelined_body(c, block_rows, h2d, compute, d2h);
+blz_status pipelined(blz_ctx* c, uint64_t block_rows, uint64_t bytes_per_block_row, H2D&& h2d, Compute&& compute,
+                     D2H&& d2h) {
+  const blz_status st = pipelined_body(c, block_rows, bytes_per_block_row, h2d, compute, d2h);
   c->stage_pieces = 1;
   const cudaError_t e1 = c->s_out ? cudaStreamSynchronize(c->s_out) : cudaSuccess;
   const cudaError_t e2 = c->s_in ? cudaStreamSynchronize(c->s_in) : cudaSuccess;
@@ -1176,7 +1190,7 @@ blz_status blz_compress_matrix(blz_ctx* c, const double* values, uint64_t rows, 
   blz_block* out_z = (blz_block*)mapped_alias(out);
   auto rows_of = [&](uint64_t b0, uint64_t b1) { return std::min(rows, 8 * b1) - 8 * b0; };
   blz_status st = pipelined(
-      c, m.block_rows,
+      c, m.block_rows, 8 * cols * sizeof(double),
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
         return xfer_h2d(c, d + 8 * b0 * cols, values + 8 * b0 * cols, rows_of(b0, b1) * cols * sizeof(double), s);
       },
@@ -1209,7 +1223,7 @@ blz_status blz_decompress_matrix(blz_ctx* c, const blz_block* in, uint64_t rows,
   const blz_block* in_z = (const blz_block*)mapped_alias(in);
   auto rows_of = [&](uint64_t b0, uint64_t b1) { return std::min(rows, 8 * b1) - 8 * b0; };
   blz_status st = pipelined(
-      c, m.block_rows,
+      c, m.block_rows, 8 * cols * sizeof(double),
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
         if (in_z) return cudaSuccess;  // read by the unpack kernel
         return xfer_h2d(c, aos_at(aos, b0, bc), in + b0 * bc, (b1 - b0) * bc * sizeof(blz_block), s);
@@ -1256,7 +1270,7 @@ static blz_status elementwise_host(blz_ctx* c, int op, const blz_block* a, const
   if (o_z) so = o_z;
   c->stage_pieces = op != 2 ? 2 : 1;
   return pipelined(
-      c, ma.block_rows,
+      c, ma.block_rows, bc * sizeof(blz_block) * (op != 2 ? 3 : 2),
       [&](uint64_t b0, uint64_t b1, cudaStream_t s) {
         const size_t n = (b1 - b0) * bc * sizeof(blz_block);
         cudaError_t e2 = cudaSuccess;
