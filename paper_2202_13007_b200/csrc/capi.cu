@@ -65,12 +65,12 @@ struct blz_ctx {
     void* p = nullptr;
     size_t bytes = 0;
   };
-  Slot slots[8];
+  Slot slots[9];
 };
 
 namespace {
 
-enum SlotId { S_ROWDOT = 0, S_IN0, S_IN1, S_OUT, S_CM0, S_CM1, S_CM2, S_AUX };
+enum SlotId { S_ROWDOT = 0, S_IN0, S_IN1, S_OUT, S_CM0, S_CM1, S_CM2, S_AUX, S_DOT };
 
 blz_status set_err(blz_ctx* c, blz_status st, const std::string& msg) {
   if (c) c->err = msg;
@@ -620,7 +620,13 @@ blz_status blz_dot_entries_dev(blz_ctx* c, const blz_cmat* a, const blz_cmat* b,
   if (blz_status st = check_cmat(c, a, "mat_dot")) return st;
   if (blz_status st = check_cmat(c, b, "mat_dot")) return st;
   if (a->cols != b->rows) return set_err(c, BLZ_INVALID_ARGUMENT, "mat_dot: inner dimension mismatch");  // :159
-  return cuda_err(c, blz::launch_dot_entries(lc(c), c->basis, view(a), view(b), i, j, n, out, 0, a->rows),
+  double* prod = nullptr;  // few queries: products spread over threads (context scratch)
+  if (n && n <= blz::kDotSplitMaxQueries && a->block_cols >= 32) {
+    cudaError_t e;
+    prod = (double*)slot(c, S_DOT, n * a->block_cols * 8 * sizeof(double), &e);
+    if (!prod) return cuda_err(c, e, "scratch allocation");
+  }
+  return cuda_err(c, blz::launch_dot_entries(lc(c), c->basis, view(a), view(b), i, j, n, out, 0, a->rows, prod),
                   "mat_dot");
 }
 

@@ -475,11 +475,104 @@ __global__ void __launch_bounds__(32) k_sum(const double* __restrict__ v, uint64
   }
 }
 
+// A handful of queries on a wide inner dimension: one thread per (query, inner
+// block t) decompresses row ri of A(bi, t) and column cj of B(t, bj) and stores the
+// eight rounded products a(ri, k) b(k, cj); then one warp per query adds them in
+// the reference's order (t ascending, k < klim) out of shared-memory batches.
+template <bool SYM>
+__global__ void __launch_bounds__(128) k_dot_products(const Basis B, CMat a, CMat b, const uint64_t* __restrict__ qi,
+                                                      const uint64_t* __restrict__ qj, uint64_t n, uint64_t row0,
+                                                      uint64_t rows_total, double* __restrict__ prod) {
+  const uint64_t total = n * a.bc;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t q = x / a.bc, t = x % a.bc;
+    const uint64_t ig = qi[q], j = qj[q];
+    if (ig >= rows_total || j >= b.cols || ig < row0 || ig - row0 >= a.rows) continue;  // k_dot_sum decides
+    const uint64_t i = ig - row0, bi = i / BD, bj = j / BD;
+    const int ri = (int)(i % BD), cj = (int)(j % BD);
+    double arow[BD], bcol[BD];
+    decompress_exact<SYM>(load_block(a, bi * a.bc + t), B, [&](int u, const double (&row)[BD]) {
+      if (u == ri) {
+#pragma unroll
+        for (int k = 0; k < BD; ++k) arow[k] = row[k];
+      }
+    });
+    decompress_exact<SYM>(load_block(b, t * b.bc + bj), B, [&](int u, const double (&row)[BD]) {
+      double v = row[0];
+#pragma unroll
+      for (int k = 1; k < BD; ++k) v = (cj == k) ? row[k] : v;
+      bcol[u] = v;
+    });
+    double* pp = prod + x * BD;
+#pragma unroll
+    for (int k = 0; k < BD; ++k) pp[k] = arow[k] * bcol[k];
+  }
+}
+
+constexpr int DOT_BATCH = 1024;  // products per shared-memory batch
+
+__global__ void __launch_bounds__(32) k_dot_sum(CMat a, CMat b, const uint64_t* __restrict__ qi,
+                                                const uint64_t* __restrict__ qj, uint64_t row0, uint64_t rows_total,
+                                                const double* __restrict__ prod, double* __restrict__ out,
+                                                unsigned long long* err) {
+  __shared__ double buf[DOT_BATCH];
+  const uint64_t q = blockIdx.x;
+  const int lane = threadIdx.x;
+  const uint64_t ig = qi[q], j = qj[q];
+  if (ig >= rows_total || j >= b.cols) {
+    if (lane == 0) {
+      latch_error(err, q, DERR_DOT_RANGE);
+      out[q] = 0.0;
+    }
+    return;
+  }
+  if (ig < row0 || ig - row0 >= a.rows) {  // another shard's row
+    if (lane == 0) out[q] = 0.0;
+    return;
+  }
+  const double* pp = prod + q * a.bc * BD;
+  const uint64_t total = a.bc * BD;
+  double r = 0.0;
+  for (uint64_t base = 0; base < total; base += DOT_BATCH) {
+    const int m = (int)(total - base < DOT_BATCH ? total - base : DOT_BATCH);
+    for (int k = lane; k < m; k += 32) buf[k] = pp[base + k];
+    __syncwarp();
+    if (lane == 0) {
+      const uint64_t t0 = base / BD;  // DOT_BATCH is a multiple of 8
+      const int nt = m / BD;
+      for (int tl = 0; tl < nt; ++tl) {
+        const uint64_t rem = a.cols - (t0 + tl) * BD;
+        const double* bp = buf + tl * BD;
+        if (rem >= BD) {
+#pragma unroll
+          for (int k = 0; k < BD; ++k) r += bp[k];
+        } else {
+          for (int k = 0; k < (int)rem; ++k) r += bp[k];  // padding columns excluded (k < klim)
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) out[q] = r;
+}
+
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out, uint64_t row0,
-                               uint64_t rows_total) {
+                               uint64_t rows_total, double* prod) {
   if (n == 0) return cudaSuccess;
   const bool sym = c.basis_sym && !c.exact_only;
+  if (prod && n <= kDotSplitMaxQueries && a.bc >= 32) {  // few queries, wide inner dimension
+    const uint64_t total = n * a.bc;
+    const unsigned g = (unsigned)((total + 127) / 128);
+    if (sym)
+      k_dot_products<true><<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, row0, rows_total, prod);
+    else
+      k_dot_products<false><<<g, 128, 0, c.stream>>>(B, a, b, i, j, n, row0, rows_total, prod);
+    k_dot_sum<<<(unsigned)n, 32, 0, c.stream>>>(a, b, i, j, row0, rows_total, prod, out, c.err);
+    *c.launches += 2;
+    return cudaGetLastError();
+  }
   if (n <= (uint64_t)c.sm_count * 64) {  // few queries: a warp per query
     const unsigned gw = (unsigned)((n + 3) / 4);
     if (sym)

@@ -74,9 +74,12 @@ cudaError_t launch_scale_fs(const LaunchCtx& c, const double* f, const double* s
 cudaError_t launch_pack_blzc(const LaunchCtx& c, const CMat& in, uint8_t* out);
 cudaError_t launch_unpack_blzc(const LaunchCtx& c, const uint8_t* in, const CMat& out, uint64_t nlimit);
 // dot.cu
+// prod (nullable): n * a.bc * 8 doubles of scratch; with it, up to
+// kDotSplitMaxQueries queries spread each query's inner blocks over threads
+constexpr uint64_t kDotSplitMaxQueries = 16;
 cudaError_t launch_dot_entries(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b,
                                const uint64_t* i, const uint64_t* j, uint64_t n, double* out, uint64_t row0,
-                               uint64_t rows_total);
+                               uint64_t rows_total, double* prod = nullptr);
 // total != null: also the ascending total of r (inside the split kernel, or by
 // k_sum after the unsplit one)
 cudaError_t launch_rowdot(const LaunchCtx& c, const Basis& B, const CMat& a, const CMat& b, double* r,
