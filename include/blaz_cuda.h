@@ -140,9 +140,11 @@ blz_status blz_scale_dev(blz_ctx* ctx, const blz_cmat* a, double c, const blz_cm
  * written instead of 45 + 45.  The result shares a's phi/C storage: it is valid
  * while a's arrays are alive and unchanged.  out may be a itself (in place). */
 blz_status blz_scale_meta_dev(blz_ctx* ctx, const blz_cmat* a, double c, blz_cmat* out);
-/* Fused op chains: the op of blz_add_dev / blz_sub_dev /
- * blz_scale_dev writing `out`, followed by blz_decompress_dev(out, dense, ld),
- * in one pass over the operands; results are bitwise those of the two calls.
+/* Op chains: the op of blz_add_dev / blz_sub_dev /
+ * blz_scale_dev writing `out`, followed by blz_decompress_dev(out, dense, ld);
+ * results are bitwise those of the two calls.  scale (and add / sub on views
+ * that are not 16-byte aligned) run as one fused pass over the operands; add /
+ * sub otherwise run their two kernels back to back, which measured faster.
  * Replaces the reference sequence mat_add(...) -> decompress_matrix(...)
  * (H/matrix.hpp:128-151, :113-126). */
 blz_status blz_add_decompress_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b, const blz_cmat* out,
@@ -216,6 +218,9 @@ blz_status blz_frobenius_allreduce_nccl(blz_ctx* ctx, void* nccl_comm, const blz
                                         const blz_cmat* b_local, double* r_local, double* total);
 blz_status blz_matmul_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local, const blz_cmat* b_local,
                            const blz_cmat* b_full, int mode, void* scratch, const blz_cmat* c_local);
+blz_status blz_dot_entries_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local, const blz_cmat* b_local,
+                                const blz_cmat* b_full, uint64_t rows_total, const uint64_t* i, const uint64_t* j,
+                                uint64_t n, double* out);
 /* Fused all-gather + decompress: a matrix held as
  * nshards (<= 16) consecutive block-row shards in separate SoA arrays --
  * typically the ranks' own shards, opened as peer pointers (CUDA IPC) so the
@@ -229,9 +234,6 @@ blz_status blz_decompress_gather_dev(blz_ctx* ctx, const blz_cmat* shards, int n
                                      uint64_t ld);
 blz_status blz_matmul_gather_dev(blz_ctx* ctx, const blz_cmat* a, const blz_cmat* b_shards, int nshards, int mode,
                                  void* scratch, const blz_cmat* out);
-blz_status blz_dot_entries_nccl(blz_ctx* ctx, void* nccl_comm, const blz_cmat* a_local, const blz_cmat* b_local,
-                                const blz_cmat* b_full, uint64_t rows_total, const uint64_t* i, const uint64_t* j,
-                                uint64_t n, double* out);
 
 /* AoS (48-byte blz_block, device memory) <-> SoA conversions. */
 blz_status blz_pack_aos_dev(blz_ctx* ctx, const blz_cmat* in, blz_block* out);
