@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(STHREADS, 2) k_gemm_simt(const double* __restr
 // (also with 2 CTAs/SM forced: 33.0), / 5-6 31.4;
 // 64x128x16 / 4 32.1; 128x32x16 / 3 30.5; 128x64x16 / 4 22.0; 64x32x32 / 3 29.5; 64x64x8 / 8 32.3;
 // XOR-swizzled unpadded tiles 32.9; grouped raster orders (4 / 8 / 16 tile-rows) 30.7; the round-1
-// 128x128x32 two-stage kernel 29.3; cuBLAS DGEMM 35.5
+// 128x128x32 two-stage kernel 29.3; register double-buffered fragments with the next tile's barrier
+// before the last k-step 31.5 (184 regs, 2 CTAs/SM) / 32.4 (capped to 3 CTAs/SM); cuBLAS DGEMM 35.5
 #ifndef G2_TM
 #define G2_TM 64
 #endif
