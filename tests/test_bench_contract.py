@@ -21,9 +21,9 @@ SMALL = ["--config", "cfg0", "--steps", "3", "--warmup", "3", "--cfg2-size", "20
          "--cfg4-size", "1024", "--e2e-steps", "2", "--cpu-sample-rows", "64", "--extra-reps", "2"]
 
 
-def _run(extra):
+def _run(extra, env=None):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + SMALL + extra, capture_output=True,
-                       text=True, timeout=900, cwd=ROOT)
+                       text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
@@ -66,3 +66,17 @@ def test_bench_reference_arm_line():
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+
+
+def test_bench_two_ranks_relaunch():
+    """--gpus 2 without a launcher re-executes under torchrun; gloo lets both ranks
+    share the one GPU for the plumbing (not for timing): the line says n_gpus 2 and
+    the sharded configs carry their bitwise cross-checks."""
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    d = _run(["--gpus", "2"], env=env)
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["parity"]["bit_exact"] is True
+    assert d["configs"]["cfg2"]["parity"]["bit_exact"] is True
+    for name in ("cfg3", "cfg4"):
+        assert d["configs"][name]["fused_peer_gather"]["equals_nccl_path"] is True
