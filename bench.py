@@ -425,7 +425,7 @@ def run_ours(args, cfg, rank, world, local):
                                     + (", captured once as a CUDA graph and replayed" if args.graph else "")),
                        "ops_timing": "per-op ms from a separate sequential pass (CUDA events between ops)"},
             "ops": op_report,
-            "roofline": {"bound": "hbm", "kernel": "k_decompress", "achieved": dec["gbs"], "peak": hbm,
+            "roofline": {"bound": "hbm", "kernel": "k_decompress_ub", "achieved": dec["gbs"], "peak": hbm,
                          "peak_kind": hbm_kind, "unit": "GB/s", "frac": dec["hbm_frac"],
                          "bytes_per_block": BYTES["decompress"], "traffic": traffic},
             "gpu_launches": int(launches),

@@ -37,6 +37,7 @@ struct blz_ctx {
   int mode = BLZ_MODE_DEFAULT;
   bool fast_ok = false;        // basis admits the verified fast path
   bool basis_sym = false;      // basis has the reference's repeated magnitudes (decompress sharing)
+  bool basis_bound = false;    // basis is the device's constant basis of the decompress kernel
   blz::FastInfo fast{};
   unsigned long long* d_stats = nullptr;  // [0] compress exact-path blocks, [1] add/sub dense fallbacks
   uint64_t* d_wl = nullptr;               // exact-path worklist: 256 B counter + capacity entries
@@ -108,6 +109,7 @@ blz::LaunchCtx lc(blz_ctx* c) {
   L.wl = c->d_wl ? c->d_wl + 32 : nullptr;
   L.stats = c->d_stats;
   L.basis_sym = c->basis_sym;
+  L.basis_bound = c->basis_bound;
   return L;
 }
 
@@ -336,6 +338,10 @@ blz_status blz_ctx_create(int device, const double* basis, blz_ctx** out) {
   else
     reference_basis(c->basis.t);
   analyse_basis(c);
+  if (blz::bind_decompress_basis(c->basis, &c->basis_bound) != cudaSuccess) {
+    blz_ctx_destroy(c);
+    return BLZ_CUDA_ERROR;
+  }
   *out = c;
   return BLZ_OK;
 }

@@ -7,6 +7,17 @@
 #include "fastpath.cuh"  // FastParams, NEED_EXACT
 #include "launch.h"
 
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+
+#ifndef DEC_UB_MINB
+#define DEC_UB_MINB 4  // CTAs of 128 per SM the register allocation targets
+#endif
+#ifndef DEC_UB_PER_THREAD
+#define DEC_UB_PER_THREAD 1  // blocks per thread of k_decompress_ub (straight-line copies; 2 / 3: 0.599 / 0.615 ms against 0.558)
+#endif
 #ifndef DEC_GRID_PER_SM
 #define DEC_GRID_PER_SM 128  // short-lived CTAs: 4 / 8 / 32 / 64 / 128 / 256 per SM: 0.589 / 0.586 / 0.575 / 0.561 / 0.560 / 0.568 ms
 #endif
@@ -143,6 +154,175 @@ __global__ void __launch_bounds__(128) k_dequantize(const Basis B, CMat in, doub
   }
 }
 
+// K2 main kernel: the basis operands of pass 2 through uniform registers.
+//
+// The record's arithmetic is decompress_rows_impl's, in the same order; what changes is
+// where the operands live.  Pass 2 walks each row in column pairs, the pair's 16 basis
+// values read from c_basis_pairs with a loop-uniform index (LDCU into uniform registers,
+// used directly as DMUL operands), so no vector registers hold basis values; the
+// integration carries the row above through a per-thread shared-memory slot.  Two things
+// keep the code in uniform control flow, which ptxas needs before it places loads in
+// uniform registers: one block per thread with no grid-stride loop, and the first column
+// pair peeled out of the rolled loop (a grid-stride loop, or the select of the first
+// pair inside it, turns the loads back into per-thread LDC).  Blocks not fully inside
+// the crop go to k_decompress_edges; an output that is not 16-byte aligned, or a context
+// whose basis is not the device's bound one, takes k_decompress (launch_decompress).
+//
+// The zero grid of s == 0 (H/codec.hpp:151) comes from the dequantized coefficients:
+// with every d(i,j) = +0.0 each pass-1 and pass-2 sum is a +0.0 first term plus +-0.0
+// products, i.e. +0.0, exactly the reference's grid.
+__constant__ double2 c_basis_pairs[4][8];  // (t(j, 2k), t(j, 2k+1)), bound per device
+
+template <bool SYM>
+__global__ void __launch_bounds__(128, DEC_UB_MINB) k_decompress_ub(const Basis B, CMat in, double* __restrict__ dense,
+                                                                    uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
+  __shared__ double2 above[4][128];  // row u-1 of this thread's block, column pairs
+  const uint64_t nb = in.nb();
+  const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x * DEC_UB_PER_THREAD + threadIdx.x;
+  RBlock recs[DEC_UB_PER_THREAD];  // every record loaded up front: the later blocks' loads
+#pragma unroll                    // overlap the earlier blocks' arithmetic
+  for (int q = 0; q < DEC_UB_PER_THREAD; ++q) recs[q] = load_block(in, min(t0 + q * blockDim.x, nb - 1));
+#pragma unroll
+  for (int q = 0; q < DEC_UB_PER_THREAD; ++q) {
+  const uint64_t t = t0 + q * blockDim.x;
+  const uint64_t tt = t < nb ? t : nb - 1;
+  const uint64_t bi = tt / in.bc, bj = tt % in.bc;
+  const RBlock& b = recs[q];
+  const uint64_t r0 = bi * BD, c0 = bj * BD;
+  const bool full = t < nb && r0 + BD <= crop_rows && c0 + BD <= crop_cols;
+
+  const double s = b.s;
+  const bool zero = (s == 0.0);
+  const double fphi = (double)b.phi;
+  double dq[KEPT];
+  if (b.phi - 1u < 255u) {
+    const double r = 1.0 / fphi;
+#pragma unroll
+    for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : dequant_d(i8_byte_to_f64(b.c[k >> 2], k & 3), fphi, r);
+  } else {
+#pragma unroll
+    for (int k = 0; k < KEPT; ++k) dq[k] = zero ? 0.0 : (double)get_coeff(b.c, k) / fphi;
+  }
+  if (SYM) {  // t(0,u) d(0,j) is the same for every u
+#pragma unroll
+    for (int j = 0; j < BD; ++j) dq[j] = B.t[0] * dq[j];
+  }
+  double* rowp = dense + r0 * ld + c0;
+#pragma unroll
+  for (int u = 0; u < BD; ++u) {
+    // idct2 pass 1 (H/dct.hpp:56-61), as decompress_rows_impl
+    double tr[BD];
+#pragma unroll
+    for (int j = 0; j < BD; ++j) {
+      double acc = SYM ? dq[j] : B.t[0 * BD + u] * dq[j];
+      acc += B.t[1 * BD + u] * dq[8 + j];
+      if (j == 0) {
+#pragma unroll
+        for (int i = 2; i < BD; ++i) acc += B.t[i * BD + u] * dq[14 + i];
+      } else if (j == 1) {
+#pragma unroll
+        for (int i = 2; i < BD; ++i) acc += B.t[i * BD + u] * dq[20 + i];
+      }
+      tr[j] = acc;
+    }
+    const double p0 = SYM ? tr[0] * B.t[0] : 0.0;  // row 0 of the basis is constant
+    double left = 0.0;
+    // idct2 pass 2 (H/dct.hpp:62-68) for columns 2k, 2k+1, then integrate_rows
+    // (H/codec.hpp:164-174) for them
+    auto pair = [&](const int k, const bool first) {
+      double a0, a1;
+      if (SYM) {
+        a0 = p0;
+        a1 = p0;
+      } else {
+        const double2 c = c_basis_pairs[k][0];
+        a0 = tr[0] * c.x;
+        a1 = tr[0] * c.y;
+      }
+#pragma unroll
+      for (int j = 1; j < BD; ++j) {
+        const double2 c = c_basis_pairs[k][j];
+        a0 += tr[j] * c.x;
+        a1 += tr[j] * c.y;
+      }
+      double x0, x1;
+      if (u == 0) {
+        x0 = first ? b.f : left + s * a0;
+        x1 = x0 + s * a1;
+      } else {
+        const double2 up = above[k][threadIdx.x];
+        x0 = first ? up.x + s * a0 : (up.x + left) / 2.0 + s * a0;
+        x1 = (up.y + x0) / 2.0 + s * a1;
+      }
+      if (u < BD - 1) above[k][threadIdx.x] = make_double2(x0, x1);
+      left = x1;
+      if (full) reinterpret_cast<double2*>(rowp)[k] = make_double2(x0, x1);
+    };
+    pair(0, true);
+#pragma unroll 1
+    for (int k = 1; k < 4; ++k) pair(k, false);
+    rowp += ld;
+  }
+  }
+}
+
+// The blocks k_decompress_ub leaves out: those partly inside the crop (the last partial
+// block-row and block-column), through the streamed per-block code with masked stores.
+template <bool SYM>
+__global__ void __launch_bounds__(128) k_decompress_edges(const Basis B, CMat in, double* __restrict__ dense,
+                                                          uint64_t ld, uint64_t crop_rows, uint64_t crop_cols,
+                                                          uint64_t er, uint64_t ec, uint64_t nvr, uint64_t nvc) {
+  // edge set: block-row er (if er < in.br) over block-columns [0, nvc), then block-column
+  // ec (if ec < in.bc) over block-rows [0, nvr) other than er
+  const uint64_t n_row = er < in.br ? nvc : 0;
+  const uint64_t n_col = ec < in.bc ? nvr - (er < nvr ? 1 : 0) : 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_row + n_col;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t bi, bj;
+    if (i < n_row) {
+      bi = er;
+      bj = i;
+    } else {
+      bi = i - n_row;
+      if (bi >= er) ++bi;
+      bj = ec;
+    }
+    const RBlock rb = load_block(in, bi * in.bc + bj);
+    const uint64_t r0 = bi * BD, c0 = bj * BD;
+    decompress_exact<SYM>(rb, B, [&](int u, const double (&row)[BD]) {
+      if (r0 + u < crop_rows) {
+#pragma unroll
+        for (int j = 0; j < BD; ++j)
+          if (c0 + j < crop_cols) dense[(r0 + u) * ld + c0 + j] = row[j];
+      }
+    });
+  }
+}
+
+// Binds the basis to c_basis_pairs of the current device: the first basis bound on a
+// device keeps the symbol (it is never rewritten, so no running kernel sees it change);
+// *bound tells whether B is that basis.
+cudaError_t bind_decompress_basis(const Basis& B, bool* bound) {
+  static std::mutex mu;
+  static std::map<int, Basis> held;
+  *bound = false;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = held.find(dev);
+  if (it == held.end()) {
+    double2 pairs[4][8];
+    for (int k = 0; k < 4; ++k)
+      for (int j = 0; j < BD; ++j) pairs[k][j] = make_double2(B.t[j * BD + 2 * k], B.t[j * BD + 2 * k + 1]);
+    e = cudaMemcpyToSymbol(c_basis_pairs, pairs, sizeof(pairs));
+    if (e != cudaSuccess) return e;
+    it = held.emplace(dev, B).first;
+  }
+  *bound = std::memcmp(it->second.t, B.t, sizeof B.t) == 0;
+  return cudaSuccess;
+}
+
 static unsigned grid_for(uint64_t n, unsigned threads, int sms, unsigned per_sm = 64) {
   const uint64_t want = (n + threads - 1) / threads;
   const uint64_t cap = (uint64_t)sms * per_sm;
@@ -191,6 +371,36 @@ cudaError_t launch_decompress_gather(const LaunchCtx& c, const Basis& B, const S
 cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
   const unsigned g = grid_for(in.nb(), 128, c.sm_count, DEC_GRID_PER_SM);
+  const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+  if (c.basis_bound && aligned && in.nb() > 0 && in.nb() / 128 < (1ull << 31)) {
+    const bool sym = c.basis_sym && !c.exact_only;
+    const unsigned g1 = (unsigned)((in.nb() + 128 * DEC_UB_PER_THREAD - 1) / (128 * DEC_UB_PER_THREAD));
+    if (sym)
+      k_decompress_ub<true><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+    else
+      k_decompress_ub<false><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+    ++*c.launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // partial blocks: block-row crop_rows/8 and block-column crop_cols/8 when the crop
+    // ends inside them
+    const uint64_t er = (crop_rows % BD) ? crop_rows / BD : ~0ull;
+    const uint64_t ec = (crop_cols % BD) ? crop_cols / BD : ~0ull;
+    if ((er < in.br) || (ec < in.bc)) {
+      const uint64_t nvr = std::min<uint64_t>(in.br, (crop_rows + BD - 1) / BD);
+      const uint64_t nvc = std::min<uint64_t>(in.bc, (crop_cols + BD - 1) / BD);
+      const uint64_t n = nvr + nvc;
+      if (sym)
+        k_decompress_edges<true><<<grid_for(n, 128, c.sm_count), 128, 0, c.stream>>>(B, in, dense, ld, crop_rows,
+                                                                                     crop_cols, er, ec, nvr, nvc);
+      else
+        k_decompress_edges<false><<<grid_for(n, 128, c.sm_count), 128, 0, c.stream>>>(B, in, dense, ld, crop_rows,
+                                                                                      crop_cols, er, ec, nvr, nvc);
+      ++*c.launches;
+      e = cudaGetLastError();
+    }
+    return e;
+  }
   if (c.basis_sym && !c.exact_only)  // exact mode keeps the plain product-per-term kernel
     k_decompress<true><<<g, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
   else

@@ -24,6 +24,7 @@ struct LaunchCtx {
   unsigned long long* wl_count;  // worklist length
   unsigned long long* stats;     // [0] compress exact-path blocks, [1] add/sub dense-fallback blocks
   bool basis_sym;                // basis has the reference's repeated magnitudes (blaz_device.cuh, BasisSym)
+  bool basis_bound;              // basis is the one bound to the device's c_basis_pairs (codec.cu)
 };
 
 // compress_pair.cu (verified fast path, two threads per block)
@@ -37,6 +38,8 @@ cudaError_t launch_compress_worklist_warp(const LaunchCtx& c, const Basis& B, co
 cudaError_t launch_compress(const LaunchCtx& c, const Basis& B, const double* dense, uint64_t rows,
                             uint64_t cols, uint64_t ld, const CMat& out);
 cudaError_t launch_dequantize(const LaunchCtx& c, const Basis& B, const CMat& in, double* tiles);
+// binds B to the current device's constant basis pairs (first basis per device wins)
+cudaError_t bind_decompress_basis(const Basis& B, bool* bound);
 cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in, double* dense,
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols);
 // A matrix held as consecutive block-row shards in separate SoA arrays (other

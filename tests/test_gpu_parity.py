@@ -948,3 +948,91 @@ def test_nccl_sharded_entry_points_one_rank():
     dev.sync()
     assert all(torch.equal(getattr(c_sh, f), getattr(c_ref, f)) for f in ("first", "slope", "coeffs", "scale"))
     lib_nccl.ncclCommDestroy(comm)
+
+
+def _np_decompress(blocks, basis, rows, cols):
+    """decompress_matrix (H/matrix.hpp:113-126) restated over numpy arrays of blocks with an
+    arbitrary basis: dequantize_prediction (H/codec.hpp:150-158, the full 8x8 grid with the
+    discarded positions as zeros), idct2 (H/dct.hpp:53-70, every product and sum rounded in
+    the reference's order), integrate_rows (H/codec.hpp:164-174).  Vectorised over blocks;
+    each array op is one IEEE binary64 operation per block."""
+    b = blocks.reshape(-1)
+    n = b.shape[0]
+    t = np.asarray(basis, np.float64).reshape(8, 8)
+    s = b["slope"]
+    d = np.zeros((n, 8, 8))
+    pos = [(0, c) for c in range(8)] + [(1, c) for c in range(8)] + [(r, 0) for r in range(2, 8)] + \
+          [(r, 1) for r in range(2, 8)]
+    phi = b["scale_factor"].astype(np.float64)
+    for k, (r, c) in enumerate(pos):
+        d[:, r, c] = b["coeffs"][:, k].astype(np.float64) / phi
+    d[s == 0.0] = 0.0
+    tmp = np.zeros((n, 8, 8))
+    for u in range(8):
+        for j in range(8):
+            acc = np.zeros(n)
+            for i in range(8):
+                acc = acc + t[i, u] * d[:, i, j]
+            tmp[:, u, j] = acc
+    x = np.zeros((n, 8, 8))
+    for u in range(8):
+        for v in range(8):
+            acc = np.zeros(n)
+            for j in range(8):
+                acc = acc + tmp[:, u, j] * t[j, v]
+            x[:, u, v] = acc
+    out = np.zeros((n, 8, 8))
+    out[:, 0, 0] = b["first"]
+    for j in range(1, 8):
+        out[:, 0, j] = out[:, 0, j - 1] + s * x[:, 0, j]
+    for i in range(1, 8):
+        out[:, i, 0] = out[:, i - 1, 0] + s * x[:, i, 0]
+        for j in range(1, 8):
+            out[:, i, j] = (out[:, i - 1, j] + out[:, i, j - 1]) / 2.0 + s * x[:, i, j]
+    br, bc = (rows + 7) // 8, (cols + 7) // 8
+    return out.reshape(br, bc, 8, 8).transpose(0, 2, 1, 3).reshape(br * 8, bc * 8)[:rows, :cols]
+
+
+@pytest.mark.parametrize("rows,cols", [(8, 8), (5, 3), (13, 8), (8, 21), (203, 141), (64, 1000), (1001, 64)])
+def test_decompress_uniform_basis_kernel_crops(port, rows, cols):
+    """k_decompress_ub stores the blocks fully inside the crop; k_decompress_edges the
+    partial last block-row / block-column.  Device API, contiguous and strided outputs."""
+    a = W.smooth_field(rows, cols, seed=rows * 7 + cols).numpy()
+    a[: min(rows, 8), : min(cols, 8)] = 0.0  # a constant (s == 0) block
+    cm = blz.compress_matrix(a)
+    want = port.decompress_matrix(cm.blocks.reshape(-1), rows, cols)
+    dcm = dev.DeviceCMat.from_host(cm)
+    got = dev.decompress(dcm)
+    wide = torch.full((rows, cols + 6), 7.0, dtype=torch.float64, device="cuda")  # ld = cols + 6
+    dev.decompress(dcm, out=wide[:, :cols])
+    odd = torch.full((rows, cols + 1), 7.0, dtype=torch.float64, device="cuda")  # ld odd: not 16-B aligned rows
+    dev.decompress(dcm, out=odd[:, :cols])
+    dev.sync()
+    for g in (got, wide[:, :cols], odd[:, :cols]):
+        assert np.array_equal(bits(g.cpu().numpy()), bits(want))
+    assert torch.all(wide[:, cols:] == 7.0) and torch.all(odd[:, cols:] == 7.0)
+    assert np.array_equal(bits(_np_decompress(cm.blocks, port.dct_basis(), rows, cols)), bits(want))
+
+
+def test_decompress_context_with_other_basis():
+    """A context whose basis is not the device's bound constant basis runs the
+    per-thread-operand kernel, with its own basis; the default context is unaffected."""
+    import ctypes as C
+
+    base = blz.default_context()
+    t = np.empty(64)
+    base.check(base.lib.blz_ctx_basis(base.handle, t.ctypes.data_as(C.c_void_p)))
+    other = t.copy()
+    other[5 * 8 + 3] = np.nextafter(other[5 * 8 + 3], 1.0)
+    other[6 * 8 + 6] *= 1.0 + 2.0 ** -40
+    ctx2 = blz.Context(basis=other)
+    try:
+        a = W.smooth_field(96, 80, seed=11).numpy()
+        cm = blz.compress_matrix(a)
+        got2 = blz.decompress_matrix(cm, ctx=ctx2)
+        got1 = blz.decompress_matrix(cm)
+        assert np.array_equal(bits(got2), bits(_np_decompress(cm.blocks, other, 96, 80)))
+        assert np.array_equal(bits(got1), bits(_np_decompress(cm.blocks, t, 96, 80)))
+        assert not np.array_equal(bits(got1), bits(got2))
+    finally:
+        ctx2.close()
