@@ -15,6 +15,9 @@
 #ifndef DEC_UB_MINB
 #define DEC_UB_MINB 4  // CTAs of 128 per SM the register allocation targets
 #endif
+#ifndef DEC_UB_STORE_AFTER
+#define DEC_UB_STORE_AFTER 2  // row stores from the shared row: 0 in the pair loop 0.558 ms, 1 after it 0.540, 2 row u-1 during row u 0.531
+#endif
 #ifndef DEC_UB_PER_THREAD
 #define DEC_UB_PER_THREAD 1  // blocks per thread of k_decompress_ub (straight-line copies; 2 / 3: 0.599 / 0.615 ms against 0.558)
 #endif
@@ -225,6 +228,12 @@ __global__ void __launch_bounds__(128, DEC_UB_MINB) k_decompress_ub(const Basis 
       }
       tr[j] = acc;
     }
+#if DEC_UB_STORE_AFTER == 2
+    if (u > 0 && full) {  // row u-1, still in the shared row until this row's pairs replace it
+#pragma unroll
+      for (int k = 0; k < 4; ++k) reinterpret_cast<double2*>(rowp - ld)[k] = above[k][threadIdx.x];
+    }
+#endif
     const double p0 = SYM ? tr[0] * B.t[0] : 0.0;  // row 0 of the basis is constant
     double left = 0.0;
     // idct2 pass 2 (H/dct.hpp:62-68) for columns 2k, 2k+1, then integrate_rows
@@ -254,15 +263,32 @@ __global__ void __launch_bounds__(128, DEC_UB_MINB) k_decompress_ub(const Basis 
         x0 = first ? up.x + s * a0 : (up.x + left) / 2.0 + s * a0;
         x1 = (up.y + x0) / 2.0 + s * a1;
       }
+#if DEC_UB_STORE_AFTER
+      above[k][threadIdx.x] = make_double2(x0, x1);
+      left = x1;
+#else
       if (u < BD - 1) above[k][threadIdx.x] = make_double2(x0, x1);
       left = x1;
       if (full) reinterpret_cast<double2*>(rowp)[k] = make_double2(x0, x1);
+#endif
     };
     pair(0, true);
 #pragma unroll 1
     for (int k = 1; k < 4; ++k) pair(k, false);
+#if DEC_UB_STORE_AFTER == 1
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) reinterpret_cast<double2*>(rowp)[k] = above[k][threadIdx.x];
+    }
+#endif
     rowp += ld;
   }
+#if DEC_UB_STORE_AFTER == 2
+  if (full) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) reinterpret_cast<double2*>(rowp - ld)[k] = above[k][threadIdx.x];
+  }
+#endif
   }
 }
 
