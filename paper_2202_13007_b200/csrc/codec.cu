@@ -18,6 +18,9 @@
 #ifndef DEC_UB_STORE_AFTER
 #define DEC_UB_STORE_AFTER 2  // row stores from the shared row: 0 in the pair loop 0.558 ms, 1 after it 0.540, 2 row u-1 during row u 0.531
 #endif
+#ifndef DEC_UB_V4
+#define DEC_UB_V4 1  // 32-byte row stores (STG.E.ENL2.256) when the output allows them: 0.531 -> 0.442 ms
+#endif
 #ifndef DEC_UB_PER_THREAD
 #define DEC_UB_PER_THREAD 1  // blocks per thread of k_decompress_ub (straight-line copies; 2 / 3: 0.599 / 0.615 ms against 0.558)
 #endif
@@ -176,7 +179,25 @@ __global__ void __launch_bounds__(128) k_dequantize(const Basis B, CMat in, doub
 // products, i.e. +0.0, exactly the reference's grid.
 __constant__ double2 c_basis_pairs[4][8];  // (t(j, 2k), t(j, 2k+1)), bound per device
 
-template <bool SYM>
+// 32-byte global store (STG.E.ENL2.256, sm_100): dst 32-byte aligned.
+__device__ __forceinline__ void st_global_v4(double* dst, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+               : "memory");
+}
+
+// Row u-1 of the block (in the shared row) to global memory: 16- or 32-byte stores.
+template <bool V4>
+__device__ __forceinline__ void store_row(double* dst, const double2 (&above)[4][128]) {
+  if (V4) {
+    st_global_v4(dst, above[0][threadIdx.x], above[1][threadIdx.x]);
+    st_global_v4(dst + 4, above[2][threadIdx.x], above[3][threadIdx.x]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) reinterpret_cast<double2*>(dst)[k] = above[k][threadIdx.x];
+  }
+}
+
+template <bool SYM, bool V4>
 __global__ void __launch_bounds__(128, DEC_UB_MINB) k_decompress_ub(const Basis B, CMat in, double* __restrict__ dense,
                                                                     uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
   __shared__ double2 above[4][128];  // row u-1 of this thread's block, column pairs
@@ -229,10 +250,7 @@ __global__ void __launch_bounds__(128, DEC_UB_MINB) k_decompress_ub(const Basis 
       tr[j] = acc;
     }
 #if DEC_UB_STORE_AFTER == 2
-    if (u > 0 && full) {  // row u-1, still in the shared row until this row's pairs replace it
-#pragma unroll
-      for (int k = 0; k < 4; ++k) reinterpret_cast<double2*>(rowp - ld)[k] = above[k][threadIdx.x];
-    }
+    if (u > 0 && full) store_row<V4>(rowp - ld, above);  // row u-1, until this row's pairs replace it
 #endif
     const double p0 = SYM ? tr[0] * B.t[0] : 0.0;  // row 0 of the basis is constant
     double left = 0.0;
@@ -284,10 +302,7 @@ __global__ void __launch_bounds__(128, DEC_UB_MINB) k_decompress_ub(const Basis 
     rowp += ld;
   }
 #if DEC_UB_STORE_AFTER == 2
-  if (full) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) reinterpret_cast<double2*>(rowp - ld)[k] = above[k][threadIdx.x];
-  }
+  if (full) store_row<V4>(rowp - ld, above);
 #endif
   }
 }
@@ -401,10 +416,15 @@ cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in
   if (c.basis_bound && aligned && in.nb() > 0 && in.nb() / 128 < (1ull << 31)) {
     const bool sym = c.basis_sym && !c.exact_only;
     const unsigned g1 = (unsigned)((in.nb() + 128 * DEC_UB_PER_THREAD - 1) / (128 * DEC_UB_PER_THREAD));
-    if (sym)
-      k_decompress_ub<true><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+    const bool v4 = DEC_UB_V4 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dense) & 31) == 0;
+    if (sym && v4)
+      k_decompress_ub<true, true><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+    else if (sym)
+      k_decompress_ub<true, false><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+    else if (v4)
+      k_decompress_ub<false, true><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
     else
-      k_decompress_ub<false><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+      k_decompress_ub<false, false><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
     ++*c.launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
