@@ -17,6 +17,10 @@
 
 #include "blaz_types.h"
 
+#ifndef DEC_V4
+#define DEC_V4 1
+#endif
+
 namespace blz {
 
 constexpr int BD = 8;
@@ -90,6 +94,48 @@ __device__ __forceinline__ double i8_byte_to_f64(uint32_t w, int q) {
 
 __device__ __forceinline__ int get_coeff(const uint32_t (&w)[7], int k) {
   return (int)(int8_t)(uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+}
+
+// One 8-double output row to global memory: two 32-byte stores (st.global.v4.f64,
+// STG.E.ENL2.256 -- whole 32-byte sectors) when v4 (dst 32-byte aligned), else four
+// 16-byte stores (dst 16-byte aligned).
+__device__ __forceinline__ void store_row8(double* dst, const double (&row)[BD], bool v4) {
+  if (v4) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * h), "d"(row[4 * h]),
+                   "d"(row[4 * h + 1]), "d"(row[4 * h + 2]), "d"(row[4 * h + 3])
+                   : "memory");
+  } else {
+    double2* d2 = reinterpret_cast<double2*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d2[q] = make_double2(row[2 * q], row[2 * q + 1]);
+  }
+}
+
+// One 8-double input row through the read-only path: two 32-byte loads
+// (ld.global.nc.v4.f64, LDG.E.ENL2.256) when v4 (src 32-byte aligned), else four 16-byte loads.
+__device__ __forceinline__ void load_row8(const double* src, double (&row)[BD], bool v4) {
+  if (v4) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+          : "=d"(row[4 * h]), "=d"(row[4 * h + 1]), "=d"(row[4 * h + 2]), "=d"(row[4 * h + 3])
+          : "l"(src + 4 * h));
+  } else {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 x = __ldg(s2 + q);
+      row[2 * q] = x.x;
+      row[2 * q + 1] = x.y;
+    }
+  }
+}
+
+// Whether rows of a dense output at `dense` with leading dimension ld take 32-byte stores.
+__device__ __host__ __forceinline__ bool rows_v4(const double* dense, uint64_t ld) {
+  return DEC_V4 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dense) & 31) == 0;
 }
 
 // Compressed block in registers.

@@ -584,23 +584,24 @@ static blz_status op_decompress_dev(blz_ctx* c, int op, const blz_cmat* a, const
   const uint64_t nb = a->block_rows * a->block_cols;
   if (nb == 0) return BLZ_OK;
   if (op == 2 && !std::isfinite(k)) return set_err(c, BLZ_INVALID_ARGUMENT, "scale: non-finite constant");
-  if (op != 2) {
-    // add / sub: since the round-2 add/sub kernel the two launches are faster than
-    // the fused kernel (0.104 + 0.564 against 0.683 ms per 16384^2), with the same
-    // bits; the fused kernel remains for scale and for unaligned views
-    const blz::CMat va = view(a), vb = view(b), vo = view(out);
-    const bool aligned = ((reinterpret_cast<uintptr_t>(va.first) | reinterpret_cast<uintptr_t>(va.coeffs) |
-                           reinterpret_cast<uintptr_t>(vb.first) | reinterpret_cast<uintptr_t>(vb.coeffs) |
-                           reinterpret_cast<uintptr_t>(vo.first) | reinterpret_cast<uintptr_t>(vo.coeffs) |
-                           reinterpret_cast<uintptr_t>(va.slope) | reinterpret_cast<uintptr_t>(vb.slope) |
-                           reinterpret_cast<uintptr_t>(vo.slope) | reinterpret_cast<uintptr_t>(va.scale) |
-                           reinterpret_cast<uintptr_t>(vb.scale) | reinterpret_cast<uintptr_t>(vo.scale)) & 15) == 0;
-    if (aligned) {
-      if (blz_status st = (op == 0 ? blz_add_dev : blz_sub_dev)(c, a, b, out)) return st;
+  // the two launches (op, then the decompress kernel) are faster than the fused kernel
+  // since the round-2 add/sub kernels and k_decompress_ub (16384^2: add 0.105 + 0.442
+  // against 0.628 ms, scale 0.067 + 0.442 against 0.533 ms), with the same bits; the
+  // fused kernel remains for views whose arrays are not 16-byte aligned
+  {
+    const blz::CMat va = view(a), vb = op == 2 ? va : view(b), vo = view(out);
+    uintptr_t bits = 0;
+    for (const blz::CMat* m : {&va, &vb, &vo})
+      bits |= reinterpret_cast<uintptr_t>(m->first) | reinterpret_cast<uintptr_t>(m->slope) |
+              reinterpret_cast<uintptr_t>(m->scale) | reinterpret_cast<uintptr_t>(m->coeffs);
+    if ((bits & 15) == 0) {
+      blz_status st = op == 0 ? blz_add_dev(c, a, b, out) : op == 1 ? blz_sub_dev(c, a, b, out) : blz_scale_dev(c, a, k, out);
+      if (st) return st;
       return blz_decompress_dev(c, out, dense, ld);
     }
-    if (blz_status st = ensure_worklist(c, nb)) return st;
   }
+  if (op != 2)
+    if (blz_status st = ensure_worklist(c, nb)) return st;
   const blz::CMat va = view(a);
   return cuda_err(c, blz::launch_op_decompress(lc(c), c->basis, op, va, op == 2 ? va : view(b), k, view(out), dense,
                                                ld, a->rows, a->cols),

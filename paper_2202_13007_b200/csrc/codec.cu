@@ -12,6 +12,9 @@
 #include <map>
 #include <mutex>
 
+#ifndef DEC_UB
+#define DEC_UB 1  // k_decompress_ub for aligned outputs (0: k_decompress everywhere; A/B builds)
+#endif
 #ifndef DEC_UB_MINB
 #define DEC_UB_MINB 4  // CTAs of 128 per SM the register allocation targets
 #endif
@@ -86,6 +89,7 @@ __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, d
   const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+  const bool v4 = rows_v4(dense, ld);
   for (uint64_t base = warp0 * 32; base < nb; base += nwarps * 32) {
     const uint64_t t = base + lane;
     const bool valid = t < nb;
@@ -96,9 +100,7 @@ __global__ void __launch_bounds__(128, 4) k_decompress(const Basis B, CMat in, d
     const bool full = valid && aligned && r0 + BD <= crop_rows && c0 + BD <= crop_cols;
     decompress_exact<SYM>(rb, B, [&](int u, const double (&row)[BD]) {
       if (full) {
-        double2* dst = reinterpret_cast<double2*>(dense + (r0 + u) * ld + c0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_double2(row[2 * q], row[2 * q + 1]);
+        store_row8(dense + (r0 + u) * ld + c0, row, v4);
       } else if (valid && r0 + u < crop_rows) {
 #pragma unroll
         for (int j = 0; j < BD; ++j)
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(128, 4) k_decompress_gather(const Basis B, con
   const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+  const bool v4 = rows_v4(dense, ld);
   for (uint64_t base = warp0 * 32; base < nb; base += nwarps * 32) {
     const uint64_t t = base + lane;
     const bool valid = t < nb;
@@ -132,9 +135,7 @@ __global__ void __launch_bounds__(128, 4) k_decompress_gather(const Basis B, con
     const bool full = valid && aligned && r0 + BD <= crop_rows && c0 + BD <= crop_cols;
     decompress_exact<SYM>(rb, B, [&](int u, const double (&row)[BD]) {
       if (full) {
-        double2* dst = reinterpret_cast<double2*>(dense + (r0 + u) * ld + c0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_double2(row[2 * q], row[2 * q + 1]);
+        store_row8(dense + (r0 + u) * ld + c0, row, v4);
       } else if (valid && r0 + u < crop_rows) {
 #pragma unroll
         for (int j = 0; j < BD; ++j)
@@ -413,7 +414,7 @@ cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
   const unsigned g = grid_for(in.nb(), 128, c.sm_count, DEC_GRID_PER_SM);
   const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
-  if (c.basis_bound && aligned && in.nb() > 0 && in.nb() / 128 < (1ull << 31)) {
+  if (DEC_UB && c.basis_bound && aligned && in.nb() > 0 && in.nb() / 128 < (1ull << 31)) {
     const bool sym = c.basis_sym && !c.exact_only;
     const unsigned g1 = (unsigned)((in.nb() + 128 * DEC_UB_PER_THREAD - 1) / (128 * DEC_UB_PER_THREAD));
     const bool v4 = DEC_UB_V4 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dense) & 31) == 0;

@@ -23,6 +23,10 @@
 #include "fastpath.cuh"
 #include "launch.h"
 
+#ifndef CMP_V4
+#define CMP_V4 1  // 32-byte tile-row loads when the input allows them
+#endif
+
 namespace blz {
 
 #ifndef CP_PAIR_WARPS
@@ -199,6 +203,7 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
   const uint64_t nb = out.nb();
   const uint64_t groups = (nb + 31) / 32;
   const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+  const bool v4 = CMP_V4 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dense) & 31) == 0;
 
   const uint64_t g0 = (uint64_t)blockIdx.x * (PAIR_WARPS / 2) + pair;
   const uint64_t gstep = (uint64_t)gridDim.x * (PAIR_WARPS / 2);
@@ -252,17 +257,12 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
 #pragma unroll
       for (int i = TR; i < 5; ++i) {
         if (i == 4 && h == 0) break;
-        const double2* row = reinterpret_cast<const double2*>(i < 4 ? p + i * ld : p - ld);
+        double x[BD];
+        load_row8(i < 4 ? p + i * ld : p - ld, x, v4);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2 x = __ldg(row + q);
-          if (i < 4) {
-            m[i * BD + 2 * q] = x.x;
-            m[i * BD + 2 * q + 1] = x.y;
-          } else {
-            up[2 * q] = x.x;
-            up[2 * q + 1] = x.y;
-          }
+        for (int j = 0; j < BD; ++j) {
+          if (i < 4) m[i * BD + j] = x[j];
+          else up[j] = x[j];
         }
       }
       asm volatile(
@@ -287,17 +287,12 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32, CP_MINB)
 #pragma unroll
       for (int i = 0; i < 5; ++i) {
         if (i == 4 && h == 0) break;
-        const double2* row = reinterpret_cast<const double2*>(i < 4 ? p + i * ld : p - ld);
+        double x[BD];
+        load_row8(i < 4 ? p + i * ld : p - ld, x, v4);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2 x = __ldg(row + q);
-          if (i < 4) {
-            m[i * BD + 2 * q] = x.x;
-            m[i * BD + 2 * q + 1] = x.y;
-          } else {
-            up[2 * q] = x.x;
-            up[2 * q + 1] = x.y;
-          }
+        for (int j = 0; j < BD; ++j) {
+          if (i < 4) m[i * BD + j] = x[j];
+          else up[j] = x[j];
         }
       }
     } else {    // edge tile: clamped rows / columns (edge replication)

@@ -24,12 +24,10 @@ template <bool SYM>
 struct Emitter {
   double* dense;
   uint64_t ld, r0, c0, crop_rows, crop_cols;
-  bool full, part;
+  bool full, part, v4;
   __device__ __forceinline__ void operator()(int u, const double (&row)[BD]) const {
     if (full) {
-      double2* dst = reinterpret_cast<double2*>(dense + (r0 + u) * ld + c0);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) dst[q] = make_double2(row[2 * q], row[2 * q + 1]);
+      store_row8(dense + (r0 + u) * ld + c0, row, v4);
     } else if (part && r0 + u < crop_rows) {
 #pragma unroll
       for (int j = 0; j < BD; ++j)
@@ -49,6 +47,7 @@ __global__ void __launch_bounds__(128, 4)
   const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
+  const bool v4 = rows_v4(dense, ld);
   for (uint64_t base = warp0 * 32; base < nb; base += nwarps * 32) {
     const uint64_t t = base + lane;
     const bool valid = t < nb;
@@ -86,7 +85,7 @@ __global__ void __launch_bounds__(128, 4)
       else store_block(out, t, r);
     }
     const uint64_t r0 = bi * BD, c0 = bj * BD;
-    Emitter<SYM> em{dense, ld, r0, c0, crop_rows, crop_cols, false, valid && !fb};
+    Emitter<SYM> em{dense, ld, r0, c0, crop_rows, crop_cols, false, valid && !fb, v4};
     em.full = em.part && aligned && r0 + BD <= crop_rows && c0 + BD <= crop_cols;
     decompress_exact<SYM>(r, B, em);
   }
@@ -103,7 +102,7 @@ __global__ void __launch_bounds__(128) k_decompress_list(const Basis B, CMat m, 
     const uint64_t t = wl[q];
     const RBlock rb = load_block(m, t);
     const uint64_t r0 = (t / m.bc) * BD, c0 = (t % m.bc) * BD;
-    Emitter<false> em{dense, ld, r0, c0, crop_rows, crop_cols, false, true};
+    Emitter<false> em{dense, ld, r0, c0, crop_rows, crop_cols, false, true, false};
     decompress_exact<false>(rb, B, em);
   }
 }
