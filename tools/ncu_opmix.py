@@ -20,7 +20,8 @@ out = subprocess.run(["ncu", "-i", args.rep, "--page", "source", "--csv", "--pri
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
 i = next(k for k, l in enumerate(lines) if l.startswith('"Address"'))
-rows = list(csv.reader(io.StringIO("\n".join(lines[i:]))))
+j = next((k for k in range(i + 1, len(lines)) if lines[k].startswith('"Kernel Name"')), len(lines))
+rows = list(csv.reader(io.StringIO("\n".join(lines[i:j]))))  # the first kernel of the report
 h = rows[0]
 ci, cs, cn = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)"), h.index("Source")
 ex, st = collections.Counter(), collections.Counter()
