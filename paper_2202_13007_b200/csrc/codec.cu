@@ -15,8 +15,11 @@
 #ifndef DEC_UB
 #define DEC_UB 1  // k_decompress_ub for aligned outputs (0: k_decompress everywhere; A/B builds)
 #endif
+#ifndef DEC_UB_THREADS
+#define DEC_UB_THREADS 32  // one-warp CTAs: 32 / 64 / 128 / 256 threads 0.4365 / 0.4386 / 0.442 / 0.463 ms
+#endif
 #ifndef DEC_UB_MINB
-#define DEC_UB_MINB 4  // CTAs of 128 per SM the register allocation targets
+#define DEC_UB_MINB (512 / DEC_UB_THREADS)  // CTAs per SM the register allocation targets (16 warps)
 #endif
 #ifndef DEC_UB_STORE_AFTER
 #define DEC_UB_STORE_AFTER 2  // row stores from the shared row: 0 in the pair loop 0.558 ms, 1 after it 0.540, 2 row u-1 during row u 0.531
@@ -188,7 +191,7 @@ __device__ __forceinline__ void st_global_v4(double* dst, double2 a, double2 b) 
 
 // Row u-1 of the block (in the shared row) to global memory: 16- or 32-byte stores.
 template <bool V4>
-__device__ __forceinline__ void store_row(double* dst, const double2 (&above)[4][128]) {
+__device__ __forceinline__ void store_row(double* dst, const double2 (&above)[4][DEC_UB_THREADS]) {
   if (V4) {
     st_global_v4(dst, above[0][threadIdx.x], above[1][threadIdx.x]);
     st_global_v4(dst + 4, above[2][threadIdx.x], above[3][threadIdx.x]);
@@ -199,9 +202,9 @@ __device__ __forceinline__ void store_row(double* dst, const double2 (&above)[4]
 }
 
 template <bool SYM, bool V4>
-__global__ void __launch_bounds__(128, DEC_UB_MINB) k_decompress_ub(const Basis B, CMat in, double* __restrict__ dense,
+__global__ void __launch_bounds__(DEC_UB_THREADS, DEC_UB_MINB) k_decompress_ub(const Basis B, CMat in, double* __restrict__ dense,
                                                                     uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
-  __shared__ double2 above[4][128];  // row u-1 of this thread's block, column pairs
+  __shared__ double2 above[4][DEC_UB_THREADS];  // row u-1 of this thread's block, column pairs
   const uint64_t nb = in.nb();
   const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x * DEC_UB_PER_THREAD + threadIdx.x;
   RBlock recs[DEC_UB_PER_THREAD];  // every record loaded up front: the later blocks' loads
@@ -414,18 +417,19 @@ cudaError_t launch_decompress(const LaunchCtx& c, const Basis& B, const CMat& in
                               uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
   const unsigned g = grid_for(in.nb(), 128, c.sm_count, DEC_GRID_PER_SM);
   const bool aligned = ((ld & 1) == 0) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0;
-  if (DEC_UB && c.basis_bound && aligned && in.nb() > 0 && in.nb() / 128 < (1ull << 31)) {
+  if (DEC_UB && c.basis_bound && aligned && in.nb() > 0 && in.nb() / DEC_UB_THREADS < (1ull << 31)) {
     const bool sym = c.basis_sym && !c.exact_only;
-    const unsigned g1 = (unsigned)((in.nb() + 128 * DEC_UB_PER_THREAD - 1) / (128 * DEC_UB_PER_THREAD));
+    constexpr uint64_t per_cta = (uint64_t)DEC_UB_THREADS * DEC_UB_PER_THREAD;
+    const unsigned g1 = (unsigned)((in.nb() + per_cta - 1) / per_cta);
     const bool v4 = DEC_UB_V4 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(dense) & 31) == 0;
     if (sym && v4)
-      k_decompress_ub<true, true><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+      k_decompress_ub<true, true><<<g1, DEC_UB_THREADS, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
     else if (sym)
-      k_decompress_ub<true, false><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+      k_decompress_ub<true, false><<<g1, DEC_UB_THREADS, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
     else if (v4)
-      k_decompress_ub<false, true><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+      k_decompress_ub<false, true><<<g1, DEC_UB_THREADS, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
     else
-      k_decompress_ub<false, false><<<g1, 128, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
+      k_decompress_ub<false, false><<<g1, DEC_UB_THREADS, 0, c.stream>>>(B, in, dense, ld, crop_rows, crop_cols);
     ++*c.launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
