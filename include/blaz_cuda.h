@@ -86,7 +86,10 @@ typedef enum blz_gemm_mode {
 int blz_abi_version(void);
 /* Creates a context on `device`.  `basis` may be NULL (the library evaluates
  * the reference expression H/dct.hpp:17-21 with the host libm) or 64 doubles
- * to upload bit-for-bit. */
+ * to upload bit-for-bit.  The first context created on a device also binds its
+ * basis to the device's constant copy used by the main decompress kernel;
+ * contexts with another basis decompress through a slower kernel (same
+ * results for their basis). */
 blz_status blz_ctx_create(int device, const double* basis, blz_ctx** out);
 void blz_ctx_destroy(blz_ctx* ctx);
 /* Stream for all subsequent calls (cudaStream_t as void*; NULL = legacy). */
