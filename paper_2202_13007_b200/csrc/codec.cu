@@ -27,6 +27,9 @@
 #ifndef DEC_UB_V4
 #define DEC_UB_V4 1  // 32-byte row stores (STG.E.ENL2.256) when the output allows them: 0.531 -> 0.442 ms
 #endif
+#ifndef DEC_UB_PF
+#define DEC_UB_PF 1184  // L2 prefetch distance of the records in CTAs (0: none; 592-2368: 0.4325 ms, none 0.4366, 4736: 0.4405)
+#endif
 #ifndef DEC_UB_PER_THREAD
 #define DEC_UB_PER_THREAD 1  // blocks per thread of k_decompress_ub (straight-line copies; 2 / 3: 0.599 / 0.615 ms against 0.558)
 #endif
@@ -201,12 +204,34 @@ __device__ __forceinline__ void store_row(double* dst, const double2 (&above)[4]
   }
 }
 
+// L2 prefetch of [p, p + n) rounded out to 16 bytes (cp.async.bulk.prefetch.L2), by the
+// threads with `on`, without a branch.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint64_t n, bool on) {
+  const uint64_t a = reinterpret_cast<uint64_t>(p) & ~15ull;
+  const uint32_t sz = (uint32_t)((reinterpret_cast<uint64_t>(p) + n + 15 - a) & ~15ull);
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+      "@q cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(a), "r"(sz), "r"((uint32_t)on)
+      : "memory");
+}
+
 template <bool SYM, bool V4>
 __global__ void __launch_bounds__(DEC_UB_THREADS, DEC_UB_MINB) k_decompress_ub(const Basis B, CMat in, double* __restrict__ dense,
                                                                     uint64_t ld, uint64_t crop_rows, uint64_t crop_cols) {
   __shared__ double2 above[4][DEC_UB_THREADS];  // row u-1 of this thread's block, column pairs
   const uint64_t nb = in.nb();
   const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x * DEC_UB_PER_THREAD + threadIdx.x;
+#if DEC_UB_PF
+  {  // the records of the CTA DEC_UB_PF CTAs ahead, into L2
+    const uint64_t p0 = (blockIdx.x + (uint64_t)DEC_UB_PF) * blockDim.x;
+    const uint64_t n = p0 < nb ? min((uint64_t)blockDim.x, nb - p0) : 0;
+    const bool on = threadIdx.x == 0 && n > 0;
+    prefetch_l2(in.first + p0, n * 8, on);
+    prefetch_l2(in.slope + p0, n * 8, on);
+    prefetch_l2(in.scale + p0, n, on);
+    prefetch_l2(in.coeffs + p0 * KEPT, n * KEPT, on);
+  }
+#endif
   RBlock recs[DEC_UB_PER_THREAD];  // every record loaded up front: the later blocks' loads
 #pragma unroll                    // overlap the earlier blocks' arithmetic
   for (int q = 0; q < DEC_UB_PER_THREAD; ++q) recs[q] = load_block(in, min(t0 + q * blockDim.x, nb - 1));
