@@ -204,14 +204,15 @@ __device__ __forceinline__ void store_row(double* dst, const double2 (&above)[4]
   }
 }
 
-// L2 prefetch of [p, p + n) rounded out to 16 bytes (cp.async.bulk.prefetch.L2), by the
-// threads with `on`, without a branch.
+// L2 prefetch of the 16-byte-aligned part of [p, p + n) (cp.async.bulk.prefetch.L2; never
+// outside the range), by the threads with `on`, without a branch.
 __device__ __forceinline__ void prefetch_l2(const void* p, uint64_t n, bool on) {
-  const uint64_t a = reinterpret_cast<uint64_t>(p) & ~15ull;
-  const uint32_t sz = (uint32_t)((reinterpret_cast<uint64_t>(p) + n + 15 - a) & ~15ull);
+  const uint64_t a = (reinterpret_cast<uint64_t>(p) + 15) & ~15ull;
+  const uint64_t e = (reinterpret_cast<uint64_t>(p) + n) & ~15ull;
+  const uint32_t sz = e > a ? (uint32_t)(e - a) : 0u;
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
-      "@q cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(a), "r"(sz), "r"((uint32_t)on)
+      "@q cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(a), "r"(sz), "r"((uint32_t)(on && sz > 0))
       : "memory");
 }
 
