@@ -19,7 +19,7 @@
 #define DEC_UB_THREADS 32  // one-warp CTAs: 32 / 64 / 128 / 256 threads 0.4365 / 0.4386 / 0.442 / 0.463 ms
 #endif
 #ifndef DEC_UB_MINB
-#define DEC_UB_MINB (512 / DEC_UB_THREADS)  // CTAs per SM the register allocation targets (16 warps)
+#define DEC_UB_MINB (640 / DEC_UB_THREADS)  // CTAs per SM the register allocation targets: 20 warps (16: 0.4327 ms, 20: 0.4293; 24 spills)
 #endif
 #ifndef DEC_UB_STORE_AFTER
 #define DEC_UB_STORE_AFTER 2  // row stores from the shared row: 0 in the pair loop 0.558 ms, 1 after it 0.540, 2 row u-1 during row u 0.531
